@@ -1,0 +1,44 @@
+"""The seeded generator: deterministic, position-addressable, planted as DESIGN.md §3 states."""
+import numpy as np
+
+import pfac_datagen as gen
+from oracle import Oracle
+
+
+def test_splitmix64_reference_values():
+    # SplitMix64 with state 0: first outputs are the published reference sequence
+    v = gen.u64(0, 0, 4)
+    assert [hex(int(x)) for x in v] == ["0xe220a8397b1dcdaf", "0x6e789e6aa1b965f4", "0x6c45d188009454f", "0xf88bb8a8724c81ec"]
+
+
+def test_text_slices_are_position_addressable():
+    full = gen.iid_text(3, 0, 10_000)
+    assert set(np.unique(full).tobytes()) <= set(b"ACGT")
+    for a, b in [(0, 1), (31, 33), (64, 4096), (9999, 10_000)]:
+        assert (gen.iid_text(3, a, b) == full[a:b]).all()
+    counts = np.bincount(np.searchsorted(np.frombuffer(b"ACGT", np.uint8), full), minlength=4)
+    assert counts.min() > 2300 and counts.max() < 2700
+
+
+def test_planting_slices_and_presence():
+    cfg = gen.CONFIGS[1]
+    P = gen.config_patterns(cfg)
+    assert len(P) == 100 and len(set(P)) == 100
+    assert all(8 <= len(p) <= 20 for p in P)
+    n = 200_000
+    full = gen.config_text(cfg, n=n, patterns=P)
+    for a, b in [(0, 5000), (4090, 12_300), (199_000, 200_000)]:
+        assert (gen.config_text(cfg, a, b, patterns=P, n=n) == full[a:b]).all()
+    # every block holds its planted pattern somewhere -> at least ~n/4096 matches
+    pos, pid = Oracle(P).match_list(full)
+    assert len(pos) >= n // 4096 - 1
+
+
+def test_config_shapes():
+    assert [len(gen.config_patterns(gen.CONFIGS[i])) for i in (1, 2)] == [100, 1000]
+    p5 = gen.config_patterns(gen.CONFIGS[5])
+    assert len(p5) == len(set(p5)) == 12 * 93 + 1000
+    t5 = gen.config_text(gen.CONFIGS[5], n=300_000)
+    # low complexity: a large fraction of positions sit inside runs
+    same = (t5[1:] == t5[:-1]).mean()
+    assert same > 0.3
