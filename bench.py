@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""PFAC hot-path benchmark (driver contract: one JSON line on rank 0).
+
+A step = one pass of the whole hot path over one batch of synthetic input
+resident in HBM: pack (ASCII -> 2-bit) -> match (PFAC walk from every position) -> compact (match
+list + count) [-> NCCL gather of counts and lists when N > 1].  Build (row 1) and the device image
+upload (row 2) happen once, before timing, and are reported as `build_ms` / `prepare_ms`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--scaling weak|strong]
+  python bench.py --impl reference ...   # the oracle (CPU) on the same workload, bounded sample
+
+Default workload: BASELINE.json configs[1] (cfg2: 256 Mbp, 1000 patterns of length 20) per GPU,
+weak scaling (each rank owns one cfg2-sized shard of a longer text; halo maxlen-1).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gbases/s per B200 and whole-box at 1/2/4/8 GPUs; % of HBM roofline"
+MATCH_BYTES_PER_BASE = 4.25   # 0.25 B packed text read + 4 B int32 out[] written
+PACK_BYTES_PER_BASE = 1.25    # 1 B ASCII read + 0.25 B packed written
+COMPACT_BYTES_PER_BASE = 4.0  # 4 B out[] read (+12 B per match written)
+FALLBACK_HBM_GBS = 6650.0     # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(cfg_idx: int):
+    """dram bytes per match launch from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"cfg{cfg_idx}", {}).get("match")
+    return None if e is None else float(e["dram_bytes_per_launch"])
+
+
+class ClockSampler:
+    """nvml SM clock + throttle reasons sampled in a thread during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(args, world, rank):
+    import pfac_datagen as gen
+    from paper_1811_10498_b200.parallel import shard
+
+    cfg = gen.CONFIGS[args.config]
+    n_total = cfg.n * world if args.scaling == "weak" else cfg.n
+    if args.n:
+        n_total = args.n * (world if args.scaling == "weak" else 1)
+    pats = gen.config_patterns(cfg)
+    maxlen = max(len(p) for p in pats)
+    sh = shard(n_total, world, rank, maxlen)
+    if cfg.repetitive:
+        text = gen.config_text(cfg, 0, sh.avail_end, patterns=pats, n=n_total)[sh.start:]
+    else:
+        text = gen.config_text(cfg, sh.start, sh.avail_end, patterns=pats, n=n_total)
+    return cfg, pats, sh, n_total, text
+
+
+def oracle_sample(pats, text, n_own, target_s):
+    """Time the oracle (as it stands, 1 core) on a prefix of this rank's text sized to ~target_s."""
+    from oracle import Oracle
+    o = Oracle(pats)
+    probe = min(n_own, 2_000_000)
+    t0 = time.perf_counter()
+    o.match_list(text, 0, probe, n=len(text))
+    rate = probe / max(time.perf_counter() - t0, 1e-6)
+    m = int(min(n_own, max(probe, rate * target_s)))
+    t0 = time.perf_counter()
+    pos, _ = o.match_list(text, 0, m, n=len(text))
+    dt = time.perf_counter() - t0
+    return m, dt, len(pos)
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import pfac_datagen as gen  # noqa: F401
+    cfg, pats, sh, n_total, text = workload(args, 1, 0)
+    from oracle import Oracle
+    o = Oracle(pats)
+    # size one step's sample so that W + K steps take about args.ref_budget seconds in total
+    probe = min(sh.n_own, 2_000_000)
+    t0 = time.perf_counter()
+    o.match_list(text, 0, probe, n=len(text))
+    rate = probe / max(time.perf_counter() - t0, 1e-6)
+    per_step = args.ref_budget / max(1, args.steps + args.warmup)
+    m = int(min(sh.n_own, max(100_000, rate * per_step)))
+    for _ in range(args.warmup):
+        o.match_list(text, 0, m, n=len(text))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.match_list(text, 0, m, n=len(text))
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = m / t / 1e9
+    sample = f"first {m} positions of the {cfg.name} text per step (walks read up to maxlen-1 further)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "Gbases/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_bases_per_step": m, "patterns": len(pats)},
+        "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "Gbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_pfac(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_10498_b200 as P
+    from paper_1811_10498_b200.parallel import gather_matches
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    t_gen = time.perf_counter()
+    cfg, pats, sh, n_total, text = workload(args, world, rank)
+    t_gen = time.perf_counter() - t_gen
+
+    t0 = time.perf_counter()
+    a = P.Automaton(pats)
+    build_ms = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    a.prepare(local)
+    prepare_ms = (time.perf_counter() - t0) * 1e3
+
+    n_own, n_avail = sh.n_own, sh.n_avail
+    h_text = torch.from_numpy(text).pin_memory()
+    d_text = h_text.to(dev)
+    packed = torch.empty(P.packed_words(n_avail), dtype=torch.int32, device=dev)
+    out = torch.empty(n_own, dtype=torch.int32, device=dev)
+    cap = n_own // 1024 + 65536
+    pos = torch.empty(cap, dtype=torch.int64, device=dev)
+    pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(P.compact_workspace_bytes(n_own), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    kernels_per_step = 3
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        P.pack_async(d_text, packed, bad, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        P.match_packed_async(a, packed, n_own, n_avail, out, stream=stream)
+        if ev is not None:
+            ev[2].record(stream)
+        P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=stream)
+        if ev is not None:
+            ev[3].record(stream)
+        if world > 1:
+            m = int(count.item())
+            gather_matches(pos, pid, min(m, cap), dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # sanity (not a parity claim; tests/ hold those): no bad byte, count fits, first out[] window
+    assert int(bad.item()) == -1
+    m_final = int(count.item())
+    assert m_final <= cap
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_ms = start.elapsed_time(end)
+    kt = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evs])  # pack, match, compact
+    t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_ms = float(t_max.item())
+    ms_per_step = t_ms / args.steps
+    value = n_total / (ms_per_step * 1e-3) / 1e9
+
+    hbm, hbm_src = peaks()
+    pack_ms, match_ms, compact_ms = (float(x) for x in kt.mean(axis=0))
+    match_gbs = MATCH_BYTES_PER_BASE * n_own / (match_ms * 1e-3) / 1e9
+    traffic = profiled_traffic(args.config) if args.n is None else None
+
+    # ---- e2e: same step from pinned HOST text, H2D + D2H of the list inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        h_pos = torch.empty(cap, dtype=torch.int64).pin_memory()
+        h_pid = torch.empty(cap, dtype=torch.int32).pin_memory()
+        h_cnt = torch.empty(1, dtype=torch.int64).pin_memory()
+        d2h = 0
+
+        def e2e_step():
+            d_text.copy_(h_text, non_blocking=True)
+            step()
+            h_cnt.copy_(count, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            mm = int(h_cnt.item())
+            h_pos[:mm].copy_(pos[:mm], non_blocking=True)
+            h_pid[:mm].copy_(pid[:mm], non_blocking=True)
+            return 8 + 12 * mm
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        for _ in range(e_steps):
+            d2h = e2e_step()
+        e2.record(stream)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([s2.elapsed_time(e2) / e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_total / (float(te.item()) * 1e-3) / 1e9, "unit": "Gbases/s",
+               "h2d_bytes_per_step": int(n_avail), "d2h_bytes_per_step": int(d2h), "steps": e_steps}
+
+    # ---- quick sanity against the oracle on rank 0 (window of out[]) + CPU baseline
+    cpu = None
+    if rank == 0:
+        from oracle import Oracle
+        w = min(n_own, 200_000)
+        assert (out[:w].cpu().numpy() == Oracle(pats).match(text, 0, w, n=n_avail)).all()
+        if world == 1 and not args.no_cpu_baseline:
+            m, dt, _ = oracle_sample(pats, text, n_own, args.cpu_seconds)
+            cpu = {"value": m / dt / 1e9, "unit": "Gbases/s", "cores": 1, "kind": "oracle",
+                   "sample": f"first {m} positions of this rank's {cfg.name} text, oracle O2 "
+                             f"(plain C, 1 thread), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gbases/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded SplitMix64 ACGT text, planted patterns; DESIGN.md §3)",
+            "config": {"workload": cfg.name, "n_bases_total": n_total, "n_bases_per_rank": n_own,
+                       "patterns": len(pats), "states": a.num_states, "max_len": a.max_len,
+                       "parallelism": f"text-sharded x{world} (halo maxlen-1)",
+                       "l2": "inputs larger than L2 (no flush): ASCII text 1 B/base, out[] 4 B/base",
+                       "matches_per_step": m_final},
+            "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": match_gbs / hbm, "traffic": traffic, "kernel": "match",
+                         "algorithmic_bytes_per_launch": MATCH_BYTES_PER_BASE * n_own, "peak_source": hbm_src},
+            "kernels_ms": {"pack": pack_ms, "match": match_ms, "compact": compact_ms,
+                           "pack_frac": PACK_BYTES_PER_BASE * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
+                           "compact_frac": COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm},
+            "match_gbases_per_s_per_gpu": n_own / (match_ms * 1e-3) / 1e9,
+            "build_ms": build_ms, "prepare_ms": prepare_ms, "gen_s": t_gen,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": kernels_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["pfac", "reference"], default="pfac")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--n", type=int, default=None, help="override bases per rank (testing)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-budget", type=float, default=60.0, help="reference arm: total seconds")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    return run_reference(args) if args.impl == "reference" else run_pfac(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,132 @@
+/*
+ * pfac.h -- C-ABI of libpfac, the B200 (sm_100a) hot path of Parallel Failure-less Aho-Corasick
+ * (PFAC) for DNA (Thambawita, Ragel, Elkaduwe, arxiv 1811.10498; cited as PAPER.md:<line>).
+ *
+ * The method (PAPER.md:91-93, Sec. IV; :204, Sec. V-B): every text position i starts its own walk
+ * of the failure-less goto automaton of the patterns over {A,C,G,T}; the walk stops at the first
+ * missing transition; out[i] is the id of the last pattern completed on the way, i.e. the id of
+ * the LONGEST pattern p with text[i .. i+|p|) = p ("PFAC can detect only the longest patterns"),
+ * or 0 if no pattern starts at i.  Pattern ids are 1-based in input order (Table 1 cell "6,1",
+ * PAPER.md:135).
+ *
+ * Conventions for every entry point:
+ *  - No call throws across the ABI or aborts; each returns PFAC_OK or a negative PFAC_E_* code
+ *    and pfac_last_error() then returns a thread-local message.
+ *  - "d_" pointers are CUDA device pointers owned by the caller (e.g. torch tensors).  The device
+ *    a call runs on is the one that owns its device buffers (found with cudaPointerGetAttributes),
+ *    independent of any runtime's "current device".
+ *  - `stream` is a cudaStream_t (CUstream) of that device, passed as void* so that this header
+ *    needs no CUDA include.  "_async" calls only enqueue work on `stream`; the other compute calls
+ *    synchronise `stream` before returning.
+ *  - Bases are the bytes A,C,G,T,a,c,g,t (case-insensitive; reading R4).
+ */
+#ifndef PFAC_H
+#define PFAC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pfac_automaton pfac_automaton; /* opaque; immutable after pfac_build */
+
+enum {
+    PFAC_OK = 0,
+    PFAC_E_ARG = -1,             /* bad argument (null, misaligned, n_avail < n_own, ...) */
+    PFAC_E_EMPTY_PATTERN = -2,   /* a pattern of length 0 (reading R3) */
+    PFAC_E_NON_ACGT = -3,        /* a pattern or text byte outside ACGTacgt (reading R5) */
+    PFAC_E_DUPLICATE = -4,       /* two equal patterns (reading R2) */
+    PFAC_E_TOO_LONG = -5,        /* a pattern longer than PFAC_MAX_LEN (reading R13) */
+    PFAC_E_TOO_MANY_STATES = -6, /* automaton would need >= 2^31 states */
+    PFAC_E_CAPACITY = -7,        /* compaction output larger than the caller's capacity */
+    PFAC_E_CUDA = -8,            /* a CUDA runtime error (message in pfac_last_error) */
+    PFAC_E_OOM = -9              /* host or device allocation failed */
+};
+
+#define PFAC_MAX_LEN 1024u
+
+/* ------------------------------------------------------------------------------------------
+ * Build (host only).  PAPER.md:120 (4 x N table over A,T,C,G), :147-149 (patterns loaded one
+ * by one, a new state per new character), Table 1.
+ *
+ * Pattern j (id j+1) is bytes[offsets[j] .. offsets[j+1]), j < k; `offsets` has k+1 entries.
+ * On success *out owns a new automaton (free with pfac_free).  Errors, checked before any work
+ * that could allocate device memory: PFAC_E_EMPTY_PATTERN, PFAC_E_NON_ACGT, PFAC_E_TOO_LONG,
+ * PFAC_E_DUPLICATE (message names both ids), PFAC_E_TOO_MANY_STATES, PFAC_E_ARG (null pointers
+ * with k > 0).  k = 0 is allowed (every out[i] is 0).
+ *
+ * Canonical numbering (the exported table): state 0 is the root; the state completing pattern p
+ * has number p (1..k); all other states get k+1, k+2, ... in breadth-first order with children
+ * visited in column order A, C, G, T.  (The paper's column order is A,T,C,G; the
+ * export uses A,C,G,T -- DESIGN.md reading R9.)
+ */
+int pfac_build(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, pfac_automaton **out);
+
+/* Frees the host tables and every device image of `a` (null is a no-op). */
+void pfac_free(pfac_automaton *a);
+
+/* Inspection (host memory owned by `a`, valid until pfac_free). */
+uint32_t pfac_num_states(const pfac_automaton *a);   /* S: states including the root */
+uint32_t pfac_num_patterns(const pfac_automaton *a); /* k */
+uint32_t pfac_max_len(const pfac_automaton *a);      /* longest pattern; walks read <= this */
+/* Canonical transition table, S*4 uint32 row-major, columns A,C,G,T; cell = next state, 0 = no
+ * transition (the root is nobody's child, so 0 is unambiguous -- the paper's "0,0" cells). */
+const uint32_t *pfac_table(const pfac_automaton *a);
+
+/* Build and upload the device image of `a` for CUDA device `device` now (otherwise it is built
+ * lazily by the first match on that device).  Returns PFAC_E_CUDA / PFAC_E_OOM on failure. */
+int pfac_prepare(const pfac_automaton *a, int device);
+
+/* ------------------------------------------------------------------------------------------
+ * Pack (step 3 of SURVEY.md Sec. 8(a)): ASCII bases -> 2-bit codes A=0,C=1,G=2,T=3, 16 bases per
+ * uint32, base j in bits 2*(j mod 16) of word j/16.  d_packed must hold pfac_packed_words(n)
+ * uint32 (a multiple of 4 words; padding words are written as 0) and be 16-byte aligned.
+ * d_first_bad (device, nullable) receives the smallest index of a byte outside ACGTacgt, or
+ * UINT64_MAX if there is none; codes of such bytes are unspecified.  Asynchronous.
+ */
+uint64_t pfac_packed_words(uint64_t n);
+int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *d_first_bad,
+                    void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Match (step 4): for every i in [0, n_own): out[i] = id of the longest pattern starting at i
+ * whose bases all lie in [0, n_avail) of the packed text, else 0.  n_avail >= n_own
+ * lets a shard see a halo of (max_len - 1) bases past its owned range (reading R6).
+ * d_packed: as written by pfac_pack_async for n_avail bases (16-byte aligned, padded);
+ * d_out: n_own int32, 16-byte aligned.  Asynchronous.
+ */
+int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own,
+                            uint64_t n_avail, int32_t *d_out, void *stream);
+
+/* Convenience: pack + validate + match over one ASCII text of n bytes (d_out: n int32).
+ * Returns PFAC_E_NON_ACGT (out[] unspecified) if the text holds a byte outside ACGTacgt, and then
+ * *first_bad (host, nullable) receives its index.  Synchronous. */
+int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out,
+               uint64_t *first_bad, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Compact (step 5): the match list {(pos_base + i, out[i]) : out[i] != 0} in ascending i.
+ * d_pos (uint64) / d_pid (uint32) receive the first min(count, capacity) entries; *count is the
+ * total.  d_hist (device, nullable): k+1 uint64 per-pattern counters, ACCUMULATED (+=) so shards
+ * and ranks can be summed; values out[i] > k are counted nowhere.
+ * pfac_compact_async: d_count is a device uint64; d_workspace holds
+ * pfac_compact_workspace_bytes(n) bytes (any content; reset by the call).  Asynchronous.
+ * pfac_compact: *count is host memory; returns PFAC_E_CAPACITY if count > capacity (the first
+ * `capacity` entries are still written).  Synchronous.
+ */
+uint64_t pfac_compact_workspace_bytes(uint64_t n);
+int pfac_compact_async(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos,
+                       uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint32_t k,
+                       uint64_t *d_hist, void *d_workspace, void *stream);
+int pfac_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos,
+                 uint32_t *d_pid, uint64_t capacity, uint64_t *count, uint32_t k, uint64_t *d_hist,
+                 void *stream);
+
+/* Thread-local message for the last non-OK return on this thread ("" if none). */
+const char *pfac_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFAC_H */

@@ -1,0 +1,203 @@
+"""Thin ctypes binding of libpfac (include/pfac.h): argument marshalling only.
+
+Every step of the path (pack, match, compact) runs in the CUDA kernels of libpfac.so; there is no
+CPU fallback.  If the library cannot be loaded the import of the op fails loudly.  torch supplies
+device memory (tensors) and streams; nothing here computes on tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+_lib = None
+
+OK, E_ARG, E_EMPTY, E_NON_ACGT, E_DUP, E_TOO_LONG, E_TOO_MANY, E_CAPACITY, E_CUDA, E_OOM = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
+MAX_LEN = 1024
+
+_SIGS = {
+    "pfac_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
+    "pfac_free": (None, [ctypes.c_void_p]),
+    "pfac_num_states": (ctypes.c_uint32, [ctypes.c_void_p]),
+    "pfac_num_patterns": (ctypes.c_uint32, [ctypes.c_void_p]),
+    "pfac_max_len": (ctypes.c_uint32, [ctypes.c_void_p]),
+    "pfac_table": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "pfac_prepare": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "pfac_packed_words": (ctypes.c_uint64, [ctypes.c_uint64]),
+    "pfac_pack_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p]),
+    "pfac_match_packed_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                               ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_match": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_compact_workspace_bytes": (ctypes.c_uint64, [ctypes.c_uint64]),
+    "pfac_compact_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_compact": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32,
+                                    ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_last_error": (ctypes.c_char_p, []),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libpfac.so (built in-tree on first use if absent)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path):
+            _build.build()
+        L = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class PfacError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        super().__init__(f"libpfac error {code}: {msg}")
+
+
+def _check(rc: int) -> None:
+    if rc != OK:
+        raise PfacError(rc, lib().pfac_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream, device) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream
+
+
+def _flatten(patterns) -> tuple[np.ndarray, np.ndarray]:
+    pats = [p.encode() if isinstance(p, str) else bytes(p) for p in patterns]
+    offs = np.zeros(len(pats) + 1, dtype=np.uint64)
+    if pats:
+        offs[1:] = np.cumsum([len(p) for p in pats])
+    data = np.frombuffer(b"".join(pats), dtype=np.uint8).copy() if pats else np.zeros(1, np.uint8)
+    return data, offs
+
+
+class Automaton:
+    """pfac_build(patterns): the BFS-ordered automaton, finals numbered as pattern ids."""
+
+    def __init__(self, patterns):
+        data, offs = _flatten(patterns)
+        h = ctypes.c_void_p()
+        _check(lib().pfac_build(data.ctypes.data, offs.ctypes.data, len(offs) - 1, ctypes.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.pfac_free(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    @property
+    def num_states(self) -> int:
+        return int(lib().pfac_num_states(self._h))
+
+    @property
+    def num_patterns(self) -> int:
+        return int(lib().pfac_num_patterns(self._h))
+
+    @property
+    def max_len(self) -> int:
+        return int(lib().pfac_max_len(self._h))
+
+    def table(self) -> np.ndarray:
+        """Canonical S x 4 table (columns A,C,G,T), copied out of the library."""
+        S = self.num_states
+        p = lib().pfac_table(self._h)
+        return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint32)), shape=(S, 4)).copy()
+
+    def prepare(self, device: int = 0) -> None:
+        _check(lib().pfac_prepare(self._h, device))
+
+
+def packed_words(n: int) -> int:
+    return int(lib().pfac_packed_words(n))
+
+
+def compact_workspace_bytes(n: int) -> int:
+    return int(lib().pfac_compact_workspace_bytes(n))
+
+
+def pack_async(text, packed=None, first_bad=None, stream=None):
+    """pfac_pack_async: uint8 CUDA tensor of n ASCII bases -> packed uint32 tensor."""
+    import torch
+    n = text.numel()
+    if packed is None:
+        packed = torch.empty(packed_words(n), dtype=torch.int32, device=text.device)
+    _check(lib().pfac_pack_async(_ptr(text), n, _ptr(packed), _ptr(first_bad), _stream(stream, text.device)))
+    return packed
+
+
+def match_packed_async(a: Automaton, packed, n_own: int, n_avail: int | None = None, out=None, stream=None):
+    """pfac_match_packed_async: out[i] for i < n_own, walks bounded by n_avail."""
+    import torch
+    n_avail = n_own if n_avail is None else n_avail
+    if out is None:
+        out = torch.empty(n_own, dtype=torch.int32, device=packed.device)
+    _check(lib().pfac_match_packed_async(a.handle, _ptr(packed), n_own, n_avail, _ptr(out),
+                                         _stream(stream, packed.device)))
+    return out
+
+
+def match(a: Automaton, text, out=None, stream=None):
+    """pfac_match: ASCII CUDA tensor -> int32 out (synchronous; raises PfacError on a non-ACGT byte)."""
+    import torch
+    n = text.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=text.device)
+    bad = ctypes.c_uint64(0)
+    _check(lib().pfac_match(a.handle, _ptr(text), n, _ptr(out), ctypes.byref(bad), _stream(stream, text.device)))
+    return out
+
+
+def compact_async(out, pos, pid, count, workspace, pos_base: int = 0, k: int = 0, hist=None, stream=None):
+    """pfac_compact_async into caller buffers (count: 1-element int64 CUDA tensor)."""
+    _check(lib().pfac_compact_async(_ptr(out), out.numel(), pos_base, _ptr(pos), _ptr(pid), pos.numel(),
+                                    _ptr(count), k, _ptr(hist), _ptr(workspace), _stream(stream, out.device)))
+
+
+def compact(out, pos_base: int = 0, capacity: int | None = None, k: int = 0, hist=None, stream=None):
+    """pfac_compact: returns (pos int64, pid int32, count) trimmed to count (synchronous)."""
+    import torch
+    n = out.numel()
+    cap = max(1024, n // 256) if capacity is None else capacity
+    while True:
+        pos = torch.empty(max(cap, 1), dtype=torch.int64, device=out.device)
+        pid = torch.empty(max(cap, 1), dtype=torch.int32, device=out.device)
+        c = ctypes.c_uint64(0)
+        rc = lib().pfac_compact(_ptr(out), n, pos_base, _ptr(pos), _ptr(pid), cap, ctypes.byref(c), k,
+                                _ptr(hist), _stream(stream, out.device))
+        if rc == E_CAPACITY and capacity is None:
+            cap = int(c.value)
+            if hist is not None:
+                raise PfacError(rc, "capacity too small with an accumulating histogram; pass capacity")
+            continue
+        _check(rc)
+        m = int(c.value)
+        return pos[:m], pid[:m], m

@@ -1,0 +1,238 @@
+// C-ABI of libpfac (declared and documented in include/pfac.h).  Argument checking, device
+// selection from the buffers' owning device, device-image upload, and error reporting.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/pfac.h"
+#include "pfac_internal.h"
+
+namespace pfac {
+static thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+static int cuda_fail(int e, const char *where) {
+    char msg[256];
+    snprintf(msg, sizeof msg, "%s: CUDA error %d (%s)", where, e, cudaGetErrorString((cudaError_t)e));
+    return fail(e == cudaErrorMemoryAllocation ? PFAC_E_OOM : PFAC_E_CUDA, msg);
+}
+
+// Make the device that owns `p` current for this runtime on this thread (torch's runtime and ours
+// keep separate "current device" state).  Returns the device or -1 if p is not device memory.
+static int device_of(const void *p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) return -1;
+    if (cudaSetDevice(attr.device) != cudaSuccess) return -1;
+    return attr.device;
+}
+
+static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// The automaton's image on `device`, uploading it on first use.
+static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
+    auto *a = const_cast<pfac_automaton *>(ca);
+    std::lock_guard<std::mutex> lock(a->mu);
+    for (DeviceImage *im : a->images)
+        if (im->device == device) {
+            *out = im;
+            return PFAC_OK;
+        }
+    const HostImage &h = a->host_image;
+    auto *im = new (std::nothrow) DeviceImage();
+    if (!im) return fail(PFAC_E_OOM, "device image: host allocation failed");
+    im->device = device;
+    im->K = h.K;
+    im->S = h.S;
+    im->deep = h.deep;
+    im->root = h.root;
+    im->maxlen = a->maxlen;
+    im->window = match_window_rows(device, h.K, a->maxlen, h.S);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_J, h.J.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_T, h.T.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_F, h.F.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(im->d_T, h.T.data(), h.T.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(im->d_J);
+        cudaFree(im->d_T);
+        cudaFree(im->d_F);
+        delete im;
+        return cuda_fail(e, "device image upload");
+    }
+    a->images.push_back(im);
+    *out = im;
+    return PFAC_OK;
+}
+}  // namespace pfac
+
+using namespace pfac;
+
+extern "C" {
+
+int pfac_build(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, pfac_automaton **out) {
+    try {
+        return build_automaton(bytes, offsets, k, out);
+    } catch (...) {
+        return fail(PFAC_E_OOM, "pfac_build: exception");
+    }
+}
+
+void pfac_free(pfac_automaton *a) {
+    if (!a) return;
+    for (DeviceImage *im : a->images) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(im->device);
+        cudaFree(im->d_J);
+        cudaFree(im->d_T);
+        cudaFree(im->d_F);
+        cudaSetDevice(prev);
+        delete im;
+    }
+    delete a;
+}
+
+uint32_t pfac_num_states(const pfac_automaton *a) { return a ? a->S : 0; }
+uint32_t pfac_num_patterns(const pfac_automaton *a) { return a ? a->k : 0; }
+uint32_t pfac_max_len(const pfac_automaton *a) { return a ? a->maxlen : 0; }
+const uint32_t *pfac_table(const pfac_automaton *a) { return a ? a->table.data() : nullptr; }
+
+int pfac_prepare(const pfac_automaton *a, int device) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_prepare: null automaton");
+    DeviceImage *im = nullptr;
+    return get_image(a, device, &im);
+}
+
+uint64_t pfac_packed_words(uint64_t n) { return (((n + 15) / 16) + 3) & ~3ull; }
+
+int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *d_first_bad, void *stream) {
+    if (n == 0) {  // nothing to pack; still report "no bad byte"
+        if (!d_first_bad) return PFAC_OK;
+        if (device_of(d_first_bad) < 0) return fail(PFAC_E_ARG, "pfac_pack_async: d_first_bad is not device memory");
+        int e = cudaMemsetAsync(d_first_bad, 0xFF, 8, (cudaStream_t)stream);
+        return e ? cuda_fail(e, "pfac_pack_async") : PFAC_OK;
+    }
+    if (!d_packed || !d_text) return fail(PFAC_E_ARG, "pfac_pack_async: null buffer");
+    if (!aligned16(d_packed)) return fail(PFAC_E_ARG, "pfac_pack_async: d_packed must be 16-byte aligned");
+    if (device_of(d_packed) < 0) return fail(PFAC_E_ARG, "pfac_pack_async: d_packed is not device memory");
+    int e = launch_pack(d_text, n, d_packed, pfac_packed_words(n), d_first_bad, stream);
+    return e ? cuda_fail(e, "pfac_pack_async") : PFAC_OK;
+}
+
+int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
+                            int32_t *d_out, void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match_packed_async: null automaton");
+    if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_packed_async: n_avail < n_own");
+    if (n_own == 0) return PFAC_OK;
+    if (!d_packed || !d_out) return fail(PFAC_E_ARG, "pfac_match_packed_async: null buffer");
+    if (!aligned16(d_packed) || !aligned16(d_out))
+        return fail(PFAC_E_ARG, "pfac_match_packed_async: d_packed and d_out must be 16-byte aligned");
+    const int dev = device_of(d_out);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match_packed_async: d_out is not device memory");
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, dev, &im);
+    if (rc) return rc;
+    int e = launch_match(*im, d_packed, n_own, n_avail, d_out, stream);
+    return e ? cuda_fail(e, "pfac_match_packed_async") : PFAC_OK;
+}
+
+int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out, uint64_t *first_bad,
+               void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match: null automaton");
+    if (n == 0) return PFAC_OK;
+    if (!d_text || !d_out) return fail(PFAC_E_ARG, "pfac_match: null buffer");
+    if (!aligned16(d_out)) return fail(PFAC_E_ARG, "pfac_match: d_out must be 16-byte aligned");
+    const int dev = device_of(d_out);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match: d_out is not device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t words = pfac_packed_words(n);
+    void *scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, words * 4 + 16, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pfac_match: scratch allocation");
+    uint32_t *d_packed = reinterpret_cast<uint32_t *>(scratch);
+    uint64_t *d_bad = reinterpret_cast<uint64_t *>(d_packed + words);
+    int rc = PFAC_OK;
+    int ce = launch_pack(d_text, n, d_packed, words, d_bad, stream);
+    uint64_t bad = ~0ull;
+    if (!ce) ce = cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st);
+    if (!ce) ce = cudaStreamSynchronize(st);
+    if (!ce && bad != ~0ull) {
+        if (first_bad) *first_bad = bad;
+        char msg[128];
+        snprintf(msg, sizeof msg, "pfac_match: text byte %llu is not one of ACGTacgt", (unsigned long long)bad);
+        rc = fail(PFAC_E_NON_ACGT, msg);
+    }
+    if (!ce && rc == PFAC_OK) {
+        DeviceImage *im = nullptr;
+        rc = get_image(a, dev, &im);
+        if (rc == PFAC_OK) {
+            ce = launch_match(*im, d_packed, n, n, d_out, stream);
+            if (!ce) ce = cudaStreamSynchronize(st);
+        }
+    }
+    cudaFreeAsync(scratch, st);
+    if (ce) return cuda_fail(ce, "pfac_match");
+    return rc;
+}
+
+uint64_t pfac_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
+
+int pfac_compact_async(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                       uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,
+                       void *stream) {
+    if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_compact_async: null d_count / d_workspace");
+    if (n > 0 && !d_out) return fail(PFAC_E_ARG, "pfac_compact_async: null d_out");
+    if (capacity > 0 && (!d_pos || !d_pid)) return fail(PFAC_E_ARG, "pfac_compact_async: null d_pos / d_pid");
+    if (n > 0 && !aligned16(d_out)) return fail(PFAC_E_ARG, "pfac_compact_async: d_out must be 16-byte aligned");
+    if (device_of(d_count) < 0) return fail(PFAC_E_ARG, "pfac_compact_async: d_count is not device memory");
+    int e = launch_compact(d_out, n, pos_base, d_pos, d_pid, capacity, d_count, k, d_hist, d_workspace, stream);
+    return e ? cuda_fail(e, "pfac_compact_async") : PFAC_OK;
+}
+
+int pfac_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                 uint64_t capacity, uint64_t *count, uint32_t k, uint64_t *d_hist, void *stream) {
+    if (!count) return fail(PFAC_E_ARG, "pfac_compact: null count");
+    if (n > 0 && !d_out) return fail(PFAC_E_ARG, "pfac_compact: null d_out");
+    const void *probe = n > 0 ? (const void *)d_out : (const void *)d_pos;
+    if (!probe || device_of(probe) < 0) return fail(PFAC_E_ARG, "pfac_compact: d_out is not device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t wsb = compact_workspace_bytes(n);
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocAsync(&ws, wsb + 8, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pfac_compact: workspace allocation");
+    uint64_t *d_count = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(ws) + wsb);
+    int rc = pfac_compact_async(d_out, n, pos_base, d_pos, d_pid, capacity, d_count, k, d_hist, ws, stream);
+    uint64_t c = 0;
+    int ce = 0;
+    if (rc == PFAC_OK) {
+        ce = cudaMemcpyAsync(&c, d_count, 8, cudaMemcpyDeviceToHost, st);
+        if (!ce) ce = cudaStreamSynchronize(st);
+    }
+    cudaFreeAsync(ws, st);
+    if (rc) return rc;
+    if (ce) return cuda_fail(ce, "pfac_compact");
+    *count = c;
+    if (c > capacity) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "pfac_compact: %llu matches > capacity %llu", (unsigned long long)c,
+                 (unsigned long long)capacity);
+        return fail(PFAC_E_CAPACITY, msg);
+    }
+    return PFAC_OK;
+}
+
+const char *pfac_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

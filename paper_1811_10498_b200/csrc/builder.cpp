@@ -1,0 +1,184 @@
+// Host automaton builder: SURVEY.md §8(a) steps 1-2 (Build, Device image).
+//
+//  1. Validate the patterns (readings R2 duplicate, R3 empty, R4 case, R5 non-ACGT, R13 length).
+//  2. Insert them one by one into a trie, a new state per new character (PAPER.md:147-149,
+//     §V-A; Table 1) -- with a fresh state for every new node (reading R1).
+//  3. Renumber canonically: root 0, the state completing pattern p gets p, every other state
+//     k+1, k+2, ... in breadth-first order, children in column order A,C,G,T (the "BFS-ordered
+//     automaton with final states numbered as pattern IDs" of BASELINE.json's north star; BFS
+//     rearrangement for locality is Nishimura et al.).
+//  4. Derive the device image: a jump table J over all K-mers, and a device
+//     numbering that puts the states at depth >= K first in BFS order so that the hot, shallow
+//     part of what the kernel walks is a prefix [0, W) that fits in shared memory.
+#include <cstdio>
+#include <deque>
+
+#include "../../include/pfac.h"
+#include "pfac_internal.h"
+
+namespace pfac {
+
+// 2-bit code of a base, A,C,G,T -> 0,1,2,3 (case-insensitive); -1 otherwise.
+static inline int base_code(uint8_t b) {
+    switch (b | 0x20) {
+        case 'a': return 0;
+        case 'c': return 1;
+        case 'g': return 2;
+        case 't': return 3;
+        default: return -1;
+    }
+}
+
+int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, pfac_automaton **out) {
+    if (!out) return fail(PFAC_E_ARG, "pfac_build: out is null");
+    *out = nullptr;
+    if (k > 0 && (!bytes || !offsets)) return fail(PFAC_E_ARG, "pfac_build: null patterns with k > 0");
+    if (k >= 0x7fffffffu) return fail(PFAC_E_TOO_MANY_STATES, "pfac_build: too many patterns");
+    char msg[256];
+    uint64_t total = 0;
+    uint32_t maxlen = 0;
+    // ---- 1. validation, before any allocation that depends on the content
+    for (uint32_t j = 0; j < k; ++j) {
+        if (offsets[j + 1] < offsets[j]) {
+            snprintf(msg, sizeof msg, "pfac_build: offsets decrease at pattern id %u", j + 1);
+            return fail(PFAC_E_ARG, msg);
+        }
+        uint64_t len = offsets[j + 1] - offsets[j];
+        if (len == 0) {
+            snprintf(msg, sizeof msg, "pfac_build: pattern id %u is empty", j + 1);
+            return fail(PFAC_E_EMPTY_PATTERN, msg);
+        }
+        if (len > PFAC_MAX_LEN) {
+            snprintf(msg, sizeof msg, "pfac_build: pattern id %u has length %llu > PFAC_MAX_LEN=%u", j + 1,
+                     (unsigned long long)len, PFAC_MAX_LEN);
+            return fail(PFAC_E_TOO_LONG, msg);
+        }
+        for (uint64_t x = offsets[j]; x < offsets[j + 1]; ++x) {
+            if (base_code(bytes[x]) < 0) {
+                snprintf(msg, sizeof msg, "pfac_build: pattern id %u has non-ACGT byte 0x%02x at offset %llu",
+                         j + 1, bytes[x], (unsigned long long)(x - offsets[j]));
+                return fail(PFAC_E_NON_ACGT, msg);
+            }
+        }
+        total += len;
+        if (len > maxlen) maxlen = (uint32_t)len;
+    }
+    // ---- 2. insertion-order trie (a new state per new character)
+    std::vector<std::array<uint32_t, 4>> child;
+    std::vector<uint32_t> fin;  // pattern id completed in this state, 0 = none
+    try {
+        child.reserve((size_t)std::min<uint64_t>(total + 1, 1ull << 28));
+        fin.reserve(child.capacity());
+    } catch (...) {
+        return fail(PFAC_E_OOM, "pfac_build: host allocation failed");
+    }
+    child.push_back({0, 0, 0, 0});
+    fin.push_back(0);
+    for (uint32_t j = 0; j < k; ++j) {
+        uint32_t s = 0;
+        for (uint64_t x = offsets[j]; x < offsets[j + 1]; ++x) {
+            int c = base_code(bytes[x]);
+            if (child[s][c] == 0) {
+                if (child.size() >= 0x7fffffffu)
+                    return fail(PFAC_E_TOO_MANY_STATES, "pfac_build: automaton needs >= 2^31 states");
+                child[s][c] = (uint32_t)child.size();
+                child.push_back({0, 0, 0, 0});
+                fin.push_back(0);
+            }
+            s = child[s][c];
+        }
+        if (fin[s] != 0) {
+            snprintf(msg, sizeof msg, "pfac_build: pattern id %u duplicates pattern id %u", j + 1, fin[s]);
+            return fail(PFAC_E_DUPLICATE, msg);
+        }
+        fin[s] = j + 1;
+    }
+    // ---- 3. canonical renumbering (BFS, finals = pattern ids)
+    auto *a = new (std::nothrow) pfac_automaton();
+    if (!a) return fail(PFAC_E_OOM, "pfac_build: host allocation failed");
+    const uint32_t S = (uint32_t)child.size();
+    a->k = k;
+    a->S = S;
+    a->maxlen = maxlen;
+    try {
+        a->table.assign((size_t)S * 4, 0);
+        a->depth.assign(S, 0);
+        a->F.assign(S, 0);
+        std::vector<uint32_t> newid(S, 0);
+        std::vector<uint32_t> order;  // insertion ids in BFS order
+        order.reserve(S);
+        order.push_back(0);
+        uint32_t next = k + 1;
+        for (size_t h = 0; h < order.size(); ++h) {
+            uint32_t u = order[h];
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v = child[u][c];
+                if (!v) continue;
+                uint32_t id = fin[v] ? fin[v] : next++;
+                newid[v] = id;
+                a->table[(size_t)newid[u] * 4 + c] = id;
+                a->depth[id] = a->depth[newid[u]] + 1;
+                a->F[id] = fin[v] ? fin[v] : a->F[newid[u]];
+                order.push_back(v);
+            }
+        }
+    } catch (...) {
+        delete a;
+        return fail(PFAC_E_OOM, "pfac_build: host allocation failed");
+    }
+    try {
+        derive_host_image(a, kJumpK);
+    } catch (...) {
+        delete a;
+        return fail(PFAC_E_OOM, "pfac_build: host allocation failed (device image)");
+    }
+    *out = a;
+    return PFAC_OK;
+}
+
+// Device image.  See DESIGN.md §5 for the layout.
+void derive_host_image(pfac_automaton *a, int K) {
+    HostImage &im = a->host_image;
+    im.K = K;
+    const uint32_t S = a->S;
+    // BFS over the canonical table from the root, children A,C,G,T
+    std::vector<uint32_t> bfs;
+    bfs.reserve(S);
+    bfs.push_back(0);
+    for (size_t h = 0; h < bfs.size(); ++h) {
+        uint32_t u = bfs[h];
+        for (int c = 0; c < 4; ++c)
+            if (uint32_t v = a->table[(size_t)u * 4 + c]) bfs.push_back(v);
+    }
+    std::vector<uint32_t> dev(S, 0);
+    uint32_t id = 1;
+    for (uint32_t u : bfs)
+        if (a->depth[u] >= (uint32_t)K) dev[u] = id++;
+    im.deep = id - 1;
+    for (uint32_t u : bfs)
+        if (a->depth[u] < (uint32_t)K) dev[u] = id++;
+    im.S = S;
+    im.root = dev[0];
+    const size_t rows = ((size_t)S + 1 + 3) & ~(size_t)3;  // padded to 4 rows for 16-byte bulk copies
+    im.T.assign(rows * 4, 0);
+    im.F.assign(rows, 0);
+    for (uint32_t u = 0; u < S; ++u) {
+        for (int c = 0; c < 4; ++c)
+            if (uint32_t v = a->table[(size_t)u * 4 + c]) im.T[(size_t)dev[u] * 4 + c] = dev[v];
+        im.F[dev[u]] = a->F[u];
+    }
+    const uint32_t nk = 1u << (2 * K);
+    im.J.assign(nk, 0);
+    for (uint32_t x = 0; x < nk; ++x) {
+        uint32_t s = 0;
+        int d = 0;
+        for (; d < K; ++d) {
+            uint32_t t = a->table[(size_t)s * 4 + ((x >> (2 * d)) & 3)];
+            if (!t) break;
+            s = t;
+        }
+        im.J[x] = (d == K) ? (kAlive | dev[s]) : a->F[s];
+    }
+}
+
+}  // namespace pfac
