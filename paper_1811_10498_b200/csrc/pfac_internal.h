@@ -25,13 +25,24 @@ struct HostImage {
     std::vector<uint32_t> F; // S+1: id of the deepest final state on the root path (0 = none)
 };
 
+// Launch plan of the match kernel for one automaton on one device (match.cu).
+struct MatchPlan {
+    uint32_t cell = 4;         // bytes per J/T/F cell: 2 (uint16, S < 32768 and k < 32768) or 4
+    bool all_smem = false;     // every T row / F entry fits in shared memory (no window check)
+    uint32_t window = 0;       // device ids [0, window) staged in shared memory
+    uint32_t slice_words = 0;  // packed words per warp slice (512 bases + halo)
+    size_t smem = 0;           // dynamic shared memory per CTA
+    int sms = 0;
+};
+
 // A device image resident on one GPU.
 struct DeviceImage {
     int device = -1;
     int K = kJumpK;
-    uint32_t S = 0, deep = 0, root = 0, window = 0;  // window: ids [0, window) staged in smem
+    uint32_t S = 0, deep = 0, root = 0;
     uint32_t maxlen = 0;
-    uint32_t *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;
+    MatchPlan plan;
+    void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
 };
 
 }  // namespace pfac
@@ -65,5 +76,5 @@ int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t
                    uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,
                    void *stream);
 uint64_t compact_workspace_bytes(uint64_t n);
-uint32_t match_window_rows(int device, int K, uint32_t maxlen, uint32_t S);
+MatchPlan plan_match(int device, int K, uint32_t maxlen, uint32_t S, uint32_t k);
 }  // namespace pfac
