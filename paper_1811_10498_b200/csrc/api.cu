@@ -53,37 +53,16 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     im->device = device;
     im->K = h.K;
     im->S = h.S;
-    im->deep = h.deep;
     im->root = h.root;
     im->maxlen = a->maxlen;
-    im->plan = plan_match(device, h.K, a->maxlen, h.S, a->k);
-    // cell width chosen by the plan: uint16 when every id fits in 15 bits, else uint32
-    std::vector<uint16_t> J16, T16, F16;
-    const void *hJ = h.J.data(), *hT = h.T.data(), *hF = h.F.data();
-    const size_t cell = im->plan.cell;
-    size_t rowsT = h.T.size() / 4, rowsF = h.F.size();
-    const size_t need = ((size_t)im->plan.window + 7) & ~(size_t)7;  // window rows must exist
-    if (rowsF < need) rowsF = need;
-    if (rowsT < need) rowsT = need;
-    if (cell == 2) {
-        J16.resize(h.J.size());
-        for (size_t i = 0; i < h.J.size(); ++i)
-            J16[i] = (uint16_t)((h.J[i] & kAlive) ? (0x8000u | (h.J[i] & 0x7FFFu)) : h.J[i]);
-        T16.assign(h.T.begin(), h.T.end());
-        F16.assign(h.F.begin(), h.F.end());
-        hJ = J16.data();
-        hT = T16.data();
-        hF = F16.data();
-    }
+    im->plan = plan_match(device, h, a->maxlen);
     cudaError_t e = cudaSetDevice(device);
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_J, h.J.size() * cell);
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_T, rowsT * 4 * cell);
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_F, rowsF * cell);
-    if (e == cudaSuccess) e = cudaMemset(im->d_T, 0, rowsT * 4 * cell);
-    if (e == cudaSuccess) e = cudaMemset(im->d_F, 0, rowsF * cell);
-    if (e == cudaSuccess) e = cudaMemcpy(im->d_J, hJ, h.J.size() * cell, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(im->d_T, hT, h.T.size() * cell, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(im->d_F, hF, h.F.size() * cell, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_J, h.J.size());
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_T, h.T.size());
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_F, h.F.size());
+    if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(im->d_J);
         cudaFree(im->d_T);

@@ -7,11 +7,10 @@
 //     k+1, k+2, ... in breadth-first order, children in column order A,C,G,T (the "BFS-ordered
 //     automaton with final states numbered as pattern IDs" of BASELINE.json's north star; BFS
 //     rearrangement for locality is Nishimura et al.).
-//  4. Derive the device image: a jump table J over all K-mers, and a device
-//     numbering that puts the states at depth >= K first in BFS order so that the hot, shallow
-//     part of what the kernel walks is a prefix [0, W) that fits in shared memory.
+//  4. Derive the device image: the same automaton renumbered chain-major, its
+//     unary runs stored as "chain rows" (up to 16 forced bases compared at once), the per-state
+//     answer F, and a jump table J over all K-mers that performs the first K steps of every walk.
 #include <cstdio>
-#include <deque>
 
 #include "../../include/pfac.h"
 #include "pfac_internal.h"
@@ -136,48 +135,93 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
     return PFAC_OK;
 }
 
-// Device image.  See DESIGN.md §5 for the layout.
+// Device image.  Layout documented on HostImage (pfac_internal.h) and in
+// chain-major ids, branch/chain rows, F, and the K-mer jump table J.
+template <typename C>
+static void put(std::vector<uint8_t> &v, size_t i, uint32_t x) {
+    reinterpret_cast<C *>(v.data())[i] = (C)x;
+}
+
 void derive_host_image(pfac_automaton *a, int K) {
     HostImage &im = a->host_image;
     im.K = K;
     const uint32_t S = a->S;
-    // BFS over the canonical table from the root, children A,C,G,T
-    std::vector<uint32_t> bfs;
-    bfs.reserve(S);
-    bfs.push_back(0);
-    for (size_t h = 0; h < bfs.size(); ++h) {
-        uint32_t u = bfs[h];
-        for (int c = 0; c < 4; ++c)
-            if (uint32_t v = a->table[(size_t)u * 4 + c]) bfs.push_back(v);
-    }
+    const uint32_t *tab = a->table.data();
+    auto nchild = [&](uint32_t u) {
+        return (uint32_t)(tab[(size_t)u * 4] != 0) + (tab[(size_t)u * 4 + 1] != 0) + (tab[(size_t)u * 4 + 2] != 0) +
+               (tab[(size_t)u * 4 + 3] != 0);
+    };
+    auto only_child = [&](uint32_t u, uint32_t &c) {
+        for (c = 0; c < 4; ++c)
+            if (tab[(size_t)u * 4 + c]) return tab[(size_t)u * 4 + c];
+        return 0u;
+    };
+    // chain-major numbering: BFS over chain heads, each head followed by its unary run
     std::vector<uint32_t> dev(S, 0);
+    std::vector<uint32_t> heads;
+    heads.reserve(1024);
+    heads.push_back(0);
     uint32_t id = 1;
-    for (uint32_t u : bfs)
-        if (a->depth[u] >= (uint32_t)K) dev[u] = id++;
-    im.deep = id - 1;
-    for (uint32_t u : bfs)
-        if (a->depth[u] < (uint32_t)K) dev[u] = id++;
+    for (size_t h = 0; h < heads.size(); ++h) {
+        uint32_t u = heads[h];
+        while (true) {
+            dev[u] = id++;
+            uint32_t c;
+            if (nchild(u) == 1) {
+                u = only_child(u, c);
+                continue;
+            }
+            for (int cc = 0; cc < 4; ++cc)
+                if (uint32_t v = tab[(size_t)u * 4 + cc]) heads.push_back(v);
+            break;
+        }
+    }
     im.S = S;
     im.root = dev[0];
-    const size_t rows = ((size_t)S + 1 + 3) & ~(size_t)3;  // padded to 4 rows for 16-byte bulk copies
-    im.T.assign(rows * 4, 0);
-    im.F.assign(rows, 0);
+    im.cell = (S < 32768u && a->k < 32768u) ? 2 : 4;
+    im.rows = ((S + 1) + 7) & ~7u;
+    const uint32_t cell = im.cell;
+    const uint32_t chain_flag = cell == 2 ? 0x8000u : 0x80000000u;
+    im.T.assign((size_t)im.rows * 4 * cell, 0);
+    im.F.assign((size_t)im.rows * cell, 0);
+    auto putc = [&](std::vector<uint8_t> &v, size_t i, uint32_t x) {
+        if (cell == 2) put<uint16_t>(v, i, x);
+        else put<uint32_t>(v, i, x);
+    };
     for (uint32_t u = 0; u < S; ++u) {
-        for (int c = 0; c < 4; ++c)
-            if (uint32_t v = a->table[(size_t)u * 4 + c]) im.T[(size_t)dev[u] * 4 + c] = dev[v];
-        im.F[dev[u]] = a->F[u];
+        const uint32_t d = dev[u];
+        putc(im.F, d, a->F[u]);
+        if (nchild(u) == 1) {  // chain row: the next L <= 16 forced bases
+            uint32_t bits = 0, L = 0, v = u, c;
+            while (L < (uint32_t)kChainMax && nchild(v) == 1) {
+                v = only_child(v, c);
+                bits |= c << (2 * L);
+                ++L;
+            }
+            putc(im.T, (size_t)d * 4 + 0, chain_flag | L);
+            if (cell == 2) {
+                putc(im.T, (size_t)d * 4 + 1, bits & 0xFFFFu);
+                putc(im.T, (size_t)d * 4 + 2, bits >> 16);
+            } else {
+                putc(im.T, (size_t)d * 4 + 1, bits);
+            }
+        } else {
+            for (int c = 0; c < 4; ++c)
+                if (uint32_t v = tab[(size_t)u * 4 + c]) putc(im.T, (size_t)d * 4 + c, dev[v]);
+        }
     }
     const uint32_t nk = 1u << (2 * K);
-    im.J.assign(nk, 0);
+    const uint32_t alive = cell == 2 ? 0x8000u : 0x80000000u;
+    im.J.assign((size_t)nk * cell, 0);
     for (uint32_t x = 0; x < nk; ++x) {
         uint32_t s = 0;
         int d = 0;
         for (; d < K; ++d) {
-            uint32_t t = a->table[(size_t)s * 4 + ((x >> (2 * d)) & 3)];
+            uint32_t t = tab[(size_t)s * 4 + ((x >> (2 * d)) & 3)];
             if (!t) break;
             s = t;
         }
-        im.J[x] = (d == K) ? (kAlive | dev[s]) : a->F[s];
+        putc(im.J, x, (d == K) ? (alive | dev[s]) : a->F[s]);
     }
 }
 

@@ -10,24 +10,33 @@
 
 namespace pfac {
 
-// Device numbering / jump table constants.
-constexpr uint32_t kAlive = 0x80000000u;  // J entry flag: walk is still alive at depth K
-constexpr int kJumpK = 7;                  // J has 4^K entries (64 KiB of uint32 in smem)
+// Device image constants.
+constexpr int kJumpK = 7;     // J has 4^K cells (uint16: 32 KiB, uint32: 64 KiB)
+constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
 
-// Host-side device image: everything the match kernel reads, before upload.
+// Host-side device image: everything the match kernel reads, already in its cell width.
+//  * Device ids 1..S number the states "chain-major": a breadth-first queue of chain heads, each
+//    head followed by its run of single-child descendants, so every unary chain has consecutive ids
+//    and shallow chains come first (the shared-memory window is a prefix of the ids).
+//  * T row of state s (4 cells): a BRANCH row holds the child id per base A,C,G,T (0 = none); a
+//    CHAIN row (s has exactly one child) holds flag|L in cell 0 and the next L <= 16 bases of the
+//    chain, 2 bits each (base i at bits 2i), in the following 32 bits.  After m matching bases the
+//    walk is in state s + m.
+//  * F[s] = pattern id of the deepest final state on the root path of s (0 = none).
+//  * J[x] for each K-mer x (base t at bits 2t): ALIVE|id of the depth-K state, or F of the deepest
+//    state the K-mer reaches when the walk dies within K bases.
 struct HostImage {
     int K = kJumpK;
-    uint32_t S = 0;          // device states, ids 1..S (row 0 is a dummy all-zero row)
-    uint32_t deep = 0;       // ids 1..deep are the states at depth >= K, breadth-first order
-    uint32_t root = 0;       // device id of the root (among the shallow ids deep+1..S)
-    std::vector<uint32_t> J; // 4^K: kAlive|id of the depth-K state, or the answer (pattern id/0)
-    std::vector<uint32_t> T; // (S+1)*4: child device id per code A,C,G,T; 0 = none
-    std::vector<uint32_t> F; // S+1: id of the deepest final state on the root path (0 = none)
+    uint32_t cell = 4;                 // bytes per cell: 2 if S < 32768 and k < 32768, else 4
+    uint32_t S = 0;                    // device ids 1..S, row 0 is an all-zero dummy
+    uint32_t root = 0;                 // device id of the root (= 1)
+    uint32_t rows = 0;                 // rows allocated (S + 1 padded to a multiple of 8)
+    std::vector<uint8_t> J, T, F;      // raw little-endian cells
 };
 
 // Launch plan of the match kernel for one automaton on one device (match.cu).
 struct MatchPlan {
-    uint32_t cell = 4;         // bytes per J/T/F cell: 2 (uint16, S < 32768 and k < 32768) or 4
+    uint32_t cell = 4;         // bytes per J/T/F cell (HostImage::cell)
     bool all_smem = false;     // every T row / F entry fits in shared memory (no window check)
     uint32_t window = 0;       // device ids [0, window) staged in shared memory
     uint32_t slice_words = 0;  // packed words per warp slice (512 bases + halo)
@@ -39,7 +48,7 @@ struct MatchPlan {
 struct DeviceImage {
     int device = -1;
     int K = kJumpK;
-    uint32_t S = 0, deep = 0, root = 0;
+    uint32_t S = 0, root = 0;
     uint32_t maxlen = 0;
     MatchPlan plan;
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
@@ -76,5 +85,5 @@ int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t
                    uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,
                    void *stream);
 uint64_t compact_workspace_bytes(uint64_t n);
-MatchPlan plan_match(int device, int K, uint32_t maxlen, uint32_t S, uint32_t k);
+MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 }  // namespace pfac
