@@ -49,7 +49,7 @@ def lib() -> ctypes.CDLL:
     """The loaded libpfac.so (built in-tree on first use if absent)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("PFAC_LIB") or _build.LIB  # PFAC_LIB: A/B experiments with another build
         if not os.path.exists(path):
             _build.build()
         L = ctypes.CDLL(path)

@@ -126,7 +126,7 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
         return fail(PFAC_E_OOM, "pfac_build: host allocation failed");
     }
     try {
-        derive_host_image(a, kJumpK);
+        derive_host_image(a);
     } catch (...) {
         delete a;
         return fail(PFAC_E_OOM, "pfac_build: host allocation failed (device image)");
@@ -142,10 +142,12 @@ static void put(std::vector<uint8_t> &v, size_t i, uint32_t x) {
     reinterpret_cast<C *>(v.data())[i] = (C)x;
 }
 
-void derive_host_image(pfac_automaton *a, int K) {
+void derive_host_image(pfac_automaton *a) {
     HostImage &im = a->host_image;
-    im.K = K;
     const uint32_t S = a->S;
+    im.cell = (S < 32768u && a->k < 32768u) ? 2 : 4;
+    const int K = im.cell == 2 ? kJumpK16 : kJumpK32;
+    im.K = K;
     const uint32_t *tab = a->table.data();
     auto nchild = [&](uint32_t u) {
         return (uint32_t)(tab[(size_t)u * 4] != 0) + (tab[(size_t)u * 4 + 1] != 0) + (tab[(size_t)u * 4 + 2] != 0) +
@@ -156,29 +158,66 @@ void derive_host_image(pfac_automaton *a, int K) {
             if (tab[(size_t)u * 4 + c]) return tab[(size_t)u * 4 + c];
         return 0u;
     };
-    // chain-major numbering: BFS over chain heads, each head followed by its unary run
+    // depth of every canonical state (BFS over the canonical table)
+    std::vector<uint32_t> depth(S, 0);
+    {
+        std::vector<uint32_t> q;
+        q.reserve(S);
+        q.push_back(0);
+        for (size_t h = 0; h < q.size(); ++h)
+            for (int c = 0; c < 4; ++c)
+                if (uint32_t v = tab[(size_t)q[h] * 4 + c]) {
+                    depth[v] = depth[q[h]] + 1;
+                    q.push_back(v);
+                }
+    }
+    // Deep-first, chain-major numbering.  Part A: the states at depth >= K, breadth-first over chain
+    // heads starting from the depth-K states (the states J hands to the kernel), each head followed
+    // by its unary run.  Part B: the states at depth < K, the same way from the root, with runs cut
+    // at depth K-1.  Runs never cross the boundary, so every chain row spans consecutive ids.
+    const uint32_t Kd = (uint32_t)K;
+    auto unary_next = [&](uint32_t u, uint32_t &v) {  // the only child of u, if u is unary and in u's part
+        uint32_t c;
+        if (nchild(u) != 1) return false;
+        v = only_child(u, c);
+        return (depth[u] + 1 >= Kd) == (depth[u] >= Kd);
+    };
     std::vector<uint32_t> dev(S, 0);
-    std::vector<uint32_t> heads;
-    heads.reserve(1024);
-    heads.push_back(0);
     uint32_t id = 1;
-    for (size_t h = 0; h < heads.size(); ++h) {
-        uint32_t u = heads[h];
-        while (true) {
-            dev[u] = id++;
-            uint32_t c;
-            if (nchild(u) == 1) {
-                u = only_child(u, c);
+    auto number_from = [&](std::vector<uint32_t> heads, bool deep) {
+        for (size_t h = 0; h < heads.size(); ++h) {
+            uint32_t u = heads[h];
+            while (true) {
+                dev[u] = id++;
+                uint32_t v;
+                if (unary_next(u, v)) {
+                    u = v;
+                    continue;
+                }
+                for (int cc = 0; cc < 4; ++cc)
+                    if (uint32_t w = tab[(size_t)u * 4 + cc])
+                        if ((depth[w] >= Kd) == deep) heads.push_back(w);
+                break;
+            }
+        }
+    };
+    {
+        std::vector<uint32_t> q, atK;
+        q.push_back(0);
+        for (size_t h = 0; h < q.size(); ++h) {
+            const uint32_t u = q[h];
+            if (depth[u] == Kd) {
+                atK.push_back(u);
                 continue;
             }
-            for (int cc = 0; cc < 4; ++cc)
-                if (uint32_t v = tab[(size_t)u * 4 + cc]) heads.push_back(v);
-            break;
+            for (int c = 0; c < 4; ++c)
+                if (uint32_t v = tab[(size_t)u * 4 + c]) q.push_back(v);
         }
+        number_from(atK, true);
+        number_from({0u}, false);
     }
     im.S = S;
     im.root = dev[0];
-    im.cell = (S < 32768u && a->k < 32768u) ? 2 : 4;
     im.rows = ((S + 1) + 7) & ~7u;
     const uint32_t cell = im.cell;
     const uint32_t chain_flag = cell == 2 ? 0x8000u : 0x80000000u;
@@ -191,19 +230,26 @@ void derive_host_image(pfac_automaton *a, int K) {
     for (uint32_t u = 0; u < S; ++u) {
         const uint32_t d = dev[u];
         putc(im.F, d, a->F[u]);
-        if (nchild(u) == 1) {  // chain row: the next L <= 16 forced bases
-            uint32_t bits = 0, L = 0, v = u, c;
-            while (L < (uint32_t)kChainMax && nchild(v) == 1) {
-                v = only_child(v, c);
+        uint32_t v0;
+        if (unary_next(u, v0)) {  // chain row: the next L <= 16 forced bases within u's part
+            uint32_t bits = 0, L = 0, v = u, c, w;
+            bool inner_final = false;  // a final state strictly inside the span (u, u+L)
+            while (L < (uint32_t)kChainMax && unary_next(v, w)) {
+                if (L > 0 && v >= 1 && v <= a->k) inner_final = true;
+                only_child(v, c);
+                v = w;
                 bits |= c << (2 * L);
                 ++L;
             }
-            putc(im.T, (size_t)d * 4 + 0, chain_flag | L);
+            const uint32_t nofin = inner_final ? 0u : (cell == 2 ? 0x4000u : 0x40000000u);
+            putc(im.T, (size_t)d * 4 + 0, chain_flag | nofin | L);
             if (cell == 2) {
                 putc(im.T, (size_t)d * 4 + 1, bits & 0xFFFFu);
                 putc(im.T, (size_t)d * 4 + 2, bits >> 16);
+                putc(im.T, (size_t)d * 4 + 3, a->F[u]);
             } else {
                 putc(im.T, (size_t)d * 4 + 1, bits);
+                putc(im.T, (size_t)d * 4 + 2, a->F[u]);
             }
         } else {
             for (int c = 0; c < 4; ++c)

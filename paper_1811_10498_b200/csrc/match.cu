@@ -8,10 +8,10 @@
 //    Lane l handles 8 consecutive positions of each 256-position sub-slice: one J lookup per
 //    position answers every walk that dies within K bases; the answers are stored right away with
 //    two coalesced st.global.cs.v4 per lane (1 KiB per warp and sub-slice).
-//  * Walks still alive after K bases continue in the automaton (the lane walks its alive positions
-//    one after the other and patches its own out[] cells).  Unary runs of the trie are "chain rows"
-//    that advance over up to 16 forced bases with one XOR, so a walk rarely needs more than one or
-//    two steps after the jump.
+//  * Positions whose walk is still alive after K bases go into a warp-private queue (one ballot per
+//    round gives each lane its slot) and are walked 32 at a time, one per lane, patching out[] after
+//    a __syncwarp.  Unary runs of the trie are "chain rows" that advance over up to 16 forced bases
+//    with one XOR, so a walk rarely needs more than one or two steps after the jump.
 // The walk itself is PAPER.md:91-93 / :204: follow the goto function from the start state, stop at
 // the first missing transition; the answer is the deepest final state passed (F).
 #include <cuda_runtime.h>
@@ -24,7 +24,14 @@
 
 namespace pfac {
 
-constexpr int kMT = 1024;                   // threads per CTA
+#ifndef PFAC_MT
+#define PFAC_MT 512
+#endif
+#ifndef PFAC_PH1_UNROLL
+#define PFAC_PH1_UNROLL 1
+#endif
+constexpr int kMT = PFAC_MT;                // threads per CTA (A/B knob)
+constexpr int kPh1Unroll = PFAC_PH1_UNROLL; // sub-slices unrolled in the lookup phase (A/B knob)
 constexpr int kMWarps = kMT / 32;
 constexpr uint32_t kP = 8;                  // consecutive positions per lane per sub-slice
 constexpr uint32_t kSubN = 32 * kP;         // 256 positions per sub-slice
@@ -48,16 +55,20 @@ template <>
 struct Row<uint16_t> {
     uint2 r;
     __device__ __forceinline__ bool chain() const { return r.x & 0x8000u; }
+    __device__ __forceinline__ bool nofin() const { return r.x & 0x4000u; }
     __device__ __forceinline__ uint32_t len() const { return r.x & 31u; }
     __device__ __forceinline__ uint32_t bits() const { return (r.x >> 16) | (r.y << 16); }
+    __device__ __forceinline__ uint32_t fin() const { return r.y >> 16; }
     __device__ __forceinline__ uint32_t child(uint32_t c) const { return ((c & 2 ? r.y : r.x) >> ((c & 1) * 16)) & 0xFFFFu; }
 };
 template <>
 struct Row<uint32_t> {
     uint4 r;
     __device__ __forceinline__ bool chain() const { return r.x & 0x80000000u; }
+    __device__ __forceinline__ bool nofin() const { return r.x & 0x40000000u; }
     __device__ __forceinline__ uint32_t len() const { return r.x & 31u; }
     __device__ __forceinline__ uint32_t bits() const { return r.y; }
+    __device__ __forceinline__ uint32_t fin() const { return r.z; }
     __device__ __forceinline__ uint32_t child(uint32_t c) const {
         return c & 2 ? (c & 1 ? r.w : r.z) : (c & 1 ? r.y : r.x);
     }
@@ -92,7 +103,8 @@ __device__ __forceinline__ uint32_t window16(const uint32_t *txt, uint32_t l) {
 
 // The PFAC walk from state s reading bases l, l+1, ... (< lend): follow the goto function until the
 // first missing transition.  A chain row advances over up to 16 forced bases with
-// one XOR; the answer is F of the last state reached (the deepest final passed).
+// one XOR; the answer is F of the last state reached (the deepest final passed).  A walk that ends
+// inside a NOFIN chain span returns the row's own F without another lookup.
 template <typename CT, bool WIN>
 __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t *txt, uint32_t s, uint32_t l,
                                          uint32_t lend) {
@@ -105,13 +117,14 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
             const uint32_t m = d ? (uint32_t)(__ffs(d) - 1) >> 1 : 16u;  // matching leading bases
             const uint32_t rem = lend - l;
             const uint32_t lim = L < rem ? L : rem;
-            if (m < lim) {
-                s += m;
+            if (m < lim || lim < L) {  // the walk ends inside this span, at s + min(m, lim)
+                const uint32_t mm = m < lim ? m : lim;
+                if (r.nofin() || mm == 0) return r.fin();
+                s += mm;
                 break;
             }
-            s += lim;
-            l += lim;
-            if (lim < L) break;
+            s += L;
+            l += L;
         } else {
             const uint32_t t = r.child(w & 3u);
             if (!t) break;
@@ -122,8 +135,10 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
     return tb.final_of(s);
 }
 
+constexpr uint32_t kQCap = 128;  // queue of alive positions (drained to < 32 before it could overflow)
+
 static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
-    return 2 * (slice_words + 4) * 4 + 16;
+    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2;
 }
 
 template <typename CT, bool WIN, int K>
@@ -144,6 +159,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint32_t *txt0 = reinterpret_cast<uint32_t *>(wbase + warp * WB);
     uint32_t *txt1 = txt0 + p.slice_words + 4;
     uint64_t *bar = reinterpret_cast<uint64_t *>(txt1 + p.slice_words + 4);
+    uint16_t *queue = reinterpret_cast<uint16_t *>(bar + 2);
+    const uint32_t lt = (1u << lane) - 1;
 
     const uint64_t TW = (uint64_t)gridDim.x * kMWarps;
     const uint64_t gw = (uint64_t)blockIdx.x * kMWarps + warp;
@@ -187,39 +204,87 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         const uint32_t lown = own_left < kSlice ? (uint32_t)own_left : kSlice;
         int32_t *out = p.out + base;
 
-#pragma unroll 1
-        for (uint32_t r = 0; r < kSub; ++r) {
-            const uint32_t l0 = r * kSubN + lane * kP;
-            if (l0 >= lown) continue;
-            uint32_t e[kP];
-            uint32_t alive = 0, x = 0;
-            if (l0 + kP - 1 + K <= lend) {  // all eight K-mers readable: one J lookup each
-                x = window16(txt, l0);
+        uint32_t qn = 0;  // warp-uniform length of the queue of alive positions
+        // Walk the queued positions 32 at a time (one per lane) until at most `keep` remain.  The
+        // __syncwarp orders the queue writes and the owners' v4 stores before these patch stores.
+        auto drain = [&](uint32_t keep) {
+            while (qn > keep) {
+                __syncwarp();
+                const uint32_t take = qn - keep < 32 ? qn - keep : 32;
+                if (lane < take) {
+                    const uint32_t l = queue[qn - take + lane];
+                    const uint32_t st = (uint32_t)sJ[window16(txt, l) & MASK] & ~ALIVE;
+                    out[l] = (int32_t)walk(tb, txt, st, l + K, lend);
+                }
+                qn -= take;
+                __syncwarp();
+            }
+        };
+        // Queue this lane's alive positions (bit r*8+j of `am` = position r*256 + lane*8 + j), one per
+        // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
+        auto push = [&](uint32_t am) {
+            while (true) {
+                const uint32_t b = __ballot_sync(~0u, am != 0);
+                if (!b) break;
+                if (qn + 32 > kQCap) drain(qn & 31);
+                if (am) {
+                    const uint32_t bit = __ffs(am) - 1;
+                    am &= am - 1;
+                    queue[qn + __popc(b & lt)] = (uint16_t)((bit >> 3) * kSubN + lane * kP + (bit & 7));
+                }
+                qn += __popc(b);
+            }
+            drain(0);
+        };
+        if (lown == kSlice && lend >= kSlice + kP - 1 + K) {
+            // interior slice: every position owned, every K-mer readable
+            uint32_t am = 0;
+#pragma unroll kPh1Unroll
+            for (uint32_t r = 0; r < kSub; ++r) {
+                const uint32_t l0 = r * kSubN + lane * kP;
+                const uint32_t x = window16(txt, l0);
+                uint32_t e[kP];
 #pragma unroll
                 for (uint32_t j = 0; j < kP; ++j) {
                     e[j] = sJ[(x >> (2 * j)) & MASK];
-                    alive |= (e[j] & ALIVE) ? (1u << j) : 0u;
+                    am |= (e[j] & ALIVE) ? (1u << (r * kP + j)) : 0u;
                 }
-            } else {  // the last bases of the readable text: plain walks from the root
-#pragma unroll
-                for (uint32_t j = 0; j < kP; ++j) e[j] = l0 + j < lend ? walk(tb, txt, p.root, l0 + j, lend) : 0u;
-            }
-            if (l0 + kP <= lown) {
-                st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);
+                st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);  // alive cells are patched by drain()
                 st_stream_v4(out + l0 + 4, e[4], e[5], e[6], e[7]);
-            } else {
+            }
+            push(am);
+        } else {
+            uint32_t am = 0;
+#pragma unroll 1
+            for (uint32_t r = 0; r < kSub; ++r) {
+                const uint32_t l0 = r * kSubN + lane * kP;
+                if (l0 >= lown) continue;
+                uint32_t e[kP];
+                uint32_t alive = 0;
+                if (l0 + kP - 1 + K <= lend) {  // all eight K-mers readable: one J lookup each
+                    const uint32_t x = window16(txt, l0);
 #pragma unroll
-                for (uint32_t j = 0; j < kP; ++j)
-                    if (l0 + j < lown) out[l0 + j] = (int32_t)e[j];
-                alive &= (1u << (lown - l0)) - 1;
+                    for (uint32_t j = 0; j < kP; ++j) {
+                        e[j] = sJ[(x >> (2 * j)) & MASK];
+                        alive |= (e[j] & ALIVE) ? (1u << j) : 0u;
+                    }
+                } else {  // the last bases of the readable text: plain walks from the root
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j)
+                        e[j] = l0 + j < lend ? walk(tb, txt, p.root, l0 + j, lend) : 0u;
+                }
+                if (l0 + kP <= lown) {
+                    st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);
+                    st_stream_v4(out + l0 + 4, e[4], e[5], e[6], e[7]);
+                } else {
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j)
+                        if (l0 + j < lown) out[l0 + j] = (int32_t)e[j];
+                    alive &= (1u << (lown - l0)) - 1;
+                }
+                am |= alive << (r * kP);
             }
-            // walks alive after K bases continue in the automaton; the same thread patches its cells
-            while (alive) {
-                const uint32_t j = __ffs(alive) - 1;
-                alive &= alive - 1;
-                const uint32_t s = (uint32_t)sJ[(x >> (2 * j)) & MASK] & ~ALIVE;
-                out[l0 + j] = (int32_t)walk(tb, txt, s, l0 + j + K, lend);
-            }
+            push(am);
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
     }
@@ -282,10 +347,10 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_ow
     const MatchPlan &pl = img.plan;
     void *args[] = {&a};
     const void *fn;
-    if (pl.cell == 2) fn = pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK>
-                                       : (const void *)match_kernel<uint16_t, true, kJumpK>;
-    else fn = pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK>
-                          : (const void *)match_kernel<uint32_t, true, kJumpK>;
+    if (pl.cell == 2) fn = pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16>
+                                       : (const void *)match_kernel<uint16_t, true, kJumpK16>;
+    else fn = pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32>
+                          : (const void *)match_kernel<uint32_t, true, kJumpK32>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     if (e != cudaSuccess) return e;
     uint64_t grid = (a.nslices + kMWarps - 1) / kMWarps;

@@ -11,22 +11,29 @@
 namespace pfac {
 
 // Device image constants.
-constexpr int kJumpK = 7;     // J has 4^K cells (uint16: 32 KiB, uint32: 64 KiB)
+#ifndef PFAC_K16
+#define PFAC_K16 8
+#endif
+constexpr int kJumpK16 = PFAC_K16;  // K for uint16 images: J has 4^8 cells = 128 KiB
+constexpr int kJumpK32 = 7;   // K for uint32 images: J has 4^7 cells = 64 KiB
 constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
 
 // Host-side device image: everything the match kernel reads, already in its cell width.
-//  * Device ids 1..S number the states "chain-major": a breadth-first queue of chain heads, each
-//    head followed by its run of single-child descendants, so every unary chain has consecutive ids
-//    and shallow chains come first (the shared-memory window is a prefix of the ids).
+//  * Device ids 1..S number the states deep-first and chain-major: first the states at depth >= K
+//    (breadth-first over chain heads starting from the depth-K states that J hands out, each head
+//    followed by its run of single-child descendants), then the states at depth < K the same way
+//    from the root.  Every chain row spans consecutive ids (runs never cross depth K), and the
+//    shared-memory window -- a prefix of the ids -- starts with the states walks resume from.
 //  * T row of state s (4 cells): a BRANCH row holds the child id per base A,C,G,T (0 = none); a
-//    CHAIN row (s has exactly one child) holds flag|L in cell 0 and the next L <= 16 bases of the
-//    chain, 2 bits each (base i at bits 2i), in the following 32 bits.  After m matching bases the
-//    walk is in state s + m.
+//    CHAIN row (s has exactly one child) holds CHAIN|NOFIN|L in cell 0, the next L <= 16 bases of
+//    the chain, 2 bits each (base i at bits 2i), in the following 32 bits, and F(s) in the last
+//    cell used (cell 3 for uint16, cell 2 for uint32).  After m matching bases the walk is in state
+//    s + m; NOFIN says no state strictly inside (s, s+L) is final, so F(s + m) = F(s) for m < L.
 //  * F[s] = pattern id of the deepest final state on the root path of s (0 = none).
 //  * J[x] for each K-mer x (base t at bits 2t): ALIVE|id of the depth-K state, or F of the deepest
 //    state the K-mer reaches when the walk dies within K bases.
 struct HostImage {
-    int K = kJumpK;
+    int K = kJumpK32;
     uint32_t cell = 4;                 // bytes per cell: 2 if S < 32768 and k < 32768, else 4
     uint32_t S = 0;                    // device ids 1..S, row 0 is an all-zero dummy
     uint32_t root = 0;                 // device id of the root (= 1)
@@ -47,7 +54,7 @@ struct MatchPlan {
 // A device image resident on one GPU.
 struct DeviceImage {
     int device = -1;
-    int K = kJumpK;
+    int K = kJumpK32;
     uint32_t S = 0, root = 0;
     uint32_t maxlen = 0;
     MatchPlan plan;
@@ -74,7 +81,7 @@ int fail(int code, const std::string &msg);
 
 // builder.cpp
 int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, pfac_automaton **out);
-void derive_host_image(pfac_automaton *a, int K);
+void derive_host_image(pfac_automaton *a);
 
 // kernels.cu launchers (all asynchronous on `stream`); return cudaError_t as int.
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,

@@ -39,10 +39,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-// Streaming (evict-first) 16-byte store: out[] is written once and never re-read by this kernel.
+// 16-byte store of out[] cells.  PFAC_OUT_STORE selects the cache hint (A/B knob): 0 = default
+// write-back (lines stay in L2 long enough for later 4-byte patches to merge), 1 = .cs evict-first.
+#ifndef PFAC_OUT_STORE
+#define PFAC_OUT_STORE 0
+#endif
 __device__ __forceinline__ void st_stream_v4(int32_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+#if PFAC_OUT_STORE == 1
     asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
+#else
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+#endif
 }
 __device__ __forceinline__ uint4 ld_stream_v4(const void *p) {
     uint4 r;
