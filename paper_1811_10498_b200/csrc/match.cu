@@ -25,7 +25,7 @@
 namespace pfac {
 
 #ifndef PFAC_MT
-#define PFAC_MT 512
+#define PFAC_MT 640
 #endif
 #ifndef PFAC_PH1_UNROLL
 #define PFAC_PH1_UNROLL 1

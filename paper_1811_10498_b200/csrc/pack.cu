@@ -29,50 +29,61 @@ __device__ __forceinline__ bool valid_byte(uint8_t b) {
     return y == 'a' || y == 'c' || y == 'g' || y == 't';
 }
 
+// A warp packs 128 consecutive words (2048 bases) per iteration: for q = 0..3 lane l reads the 16
+// bytes of word 32q + l (one coalesced 512-byte load per q) and writes that word (a coalesced
+// 128-byte store per q).  Grid-stride over the padded word range.
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t *__restrict__ text, uint64_t n,
-                                                   uint32_t *__restrict__ packed, uint64_t ngroups,
+                                                   uint32_t *__restrict__ packed, uint64_t nwords,
                                                    uint64_t *first_bad, bool aligned) {
-    // one group = 4 packed words = 64 bases; grid-stride
-    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < ngroups;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t b0 = g * 64;
-        uint32_t w[4];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t wb = warp * 128; wb < nwords; wb += nwarps * 128) {
         bool ok = true;
-        if (aligned && b0 + 64 <= n) {
+        if (aligned && (wb + 128) * 16 <= n) {
+            uint4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = ld_stream_v4(text + (wb + 32 * q + lane) * 16);
             uint32_t m = 0xFFFFFFFFu;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                uint4 v = ld_stream_v4(text + b0 + 16 * q);
-                m &= valid4(v.x) & valid4(v.y) & valid4(v.z) & valid4(v.w);
-                w[q] = pack4(v.x) | (pack4(v.y) << 8) | (pack4(v.z) << 16) | (pack4(v.w) << 24);
+                m &= valid4(v[q].x) & valid4(v[q].y) & valid4(v[q].z) & valid4(v[q].w);
+                packed[wb + 32 * q + lane] =
+                    pack4(v[q].x) | (pack4(v[q].y) << 8) | (pack4(v[q].z) << 16) | (pack4(v[q].w) << 24);
             }
             ok = (m == 0xFFFFFFFFu);
         } else {
-#pragma unroll
+#pragma unroll 1
             for (int q = 0; q < 4; ++q) {
+                const uint64_t w = wb + 32 * q + lane;
+                if (w >= nwords) break;
                 uint32_t word = 0;
                 for (int j = 0; j < 16; ++j) {
-                    uint64_t i = b0 + 16 * q + j;
+                    const uint64_t i = w * 16 + j;
                     if (i < n) {
-                        uint8_t b = text[i];
+                        const uint8_t b = text[i];
                         ok &= valid_byte(b);
-                        uint32_t t = (b >> 1) & 3u;
+                        const uint32_t t = (b >> 1) & 3u;
                         word |= (t ^ (t >> 1)) << (2 * j);
                     }
                 }
-                w[q] = word;
+                packed[w] = word;
             }
         }
-        if (!ok && first_bad) {
-            for (int j = 0; j < 64; ++j) {
-                uint64_t i = b0 + j;
-                if (i < n && !valid_byte(text[i])) {
-                    atomicMin(reinterpret_cast<unsigned long long *>(first_bad), (unsigned long long)i);
-                    break;
+        if (!ok && first_bad) {  // rare: locate this lane's first bad byte exactly
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t w = wb + 32 * q + lane;
+                bool found = false;
+                for (int j = 0; j < 16 && !found; ++j) {
+                    const uint64_t i = w * 16 + j;
+                    if (i < n && !valid_byte(text[i])) {
+                        atomicMin(reinterpret_cast<unsigned long long *>(first_bad), (unsigned long long)i);
+                        found = true;
+                    }
                 }
+                if (found) break;
             }
         }
-        *reinterpret_cast<uint4 *>(packed + 4 * g) = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -83,16 +94,15 @@ int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t 
         cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, sizeof(uint64_t), st);
         if (e != cudaSuccess) return e;
     }
-    const uint64_t ngroups = nwords_padded / 4;
-    if (ngroups == 0) return cudaSuccess;
+    if (nwords_padded == 0) return cudaSuccess;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint64_t blocks = (ngroups + 255) / 256;
+    uint64_t blocks = (nwords_padded + 1023) / 1024;  // 8 warps x 128 words per block and pass
     const uint64_t cap = (uint64_t)sms * 8;
     if (blocks > cap) blocks = cap;
     const bool aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
-    pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_text, n, d_packed, ngroups, d_first_bad, aligned);
+    pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_text, n, d_packed, nwords_padded, d_first_bad, aligned);
     return cudaGetLastError();
 }
 

@@ -1,5 +1,5 @@
 # usage: bash scripts/ab.sh [bench args] -- runs bench.py with the default lib and each alt lib
-for lib in "" paper_1811_10498_b200/_lib/alt/*.so; do
+for lib in "" $(ls paper_1811_10498_b200/_lib/alt/*.so 2>/dev/null); do
   echo "== lib: ${lib:-default}"
   PFAC_LIB=$lib timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e "$@" | python -c "
 import json,sys
