@@ -11,18 +11,18 @@ namespace pfac {
 
 // ============================================================================ pack
 // ASCII -> 2-bit codes (A0 C1 G2 T3), 16 bases per uint32, base j at bits 2(j mod 16).
-// (b >> 1) & 3 gives A0 C1 T2 G3 for upper and lower case; t ^ (t >> 1) swaps G and T.
-__device__ __forceinline__ uint32_t pack4(uint32_t x) {
-    uint32_t t = (x >> 1) & 0x03030303u;
-    uint32_t c = t ^ ((t >> 1) & 0x01010101u);
-    c = (c | (c >> 6)) & 0x000F000Fu;
-    return (c | (c >> 12)) & 0xFFu;
-}
-// 0xFF in each byte lane that holds one of ACGTacgt.
-__device__ __forceinline__ uint32_t valid4(uint32_t x) {
-    uint32_t y = x | 0x20202020u;
-    return __vcmpeq4(y, 0x61616161u) | __vcmpeq4(y, 0x63636363u) | __vcmpeq4(y, 0x67676767u) |
-           __vcmpeq4(y, 0x74747474u);
+// Four bytes at a time (one 32-bit word x):
+//   t = (x >> 1) & 3 per byte gives A0 C1 T2 G3 for upper and lower case;
+//   validity: the byte must equal "acgt"[t] after |0x20 -- one PRMT builds the expected word;
+//   code = t ^ (t >> 1) swaps G and T; one multiply gathers the four 2-bit codes into a byte.
+// Integer ALU (LOP3/SHF/PRMT) is the scarce pipe here (half rate), so the multiply does the gather.
+__device__ __forceinline__ uint32_t pack4(uint32_t x, uint32_t &bad) {
+    const uint32_t t = (x >> 1) & 0x03030303u;
+    uint32_t sel = t | (t >> 4);                    // nibble selectors at bits 0, 4, 16, 20
+    sel = (sel & 0xFFu) | ((sel >> 8) & 0xFF00u);   // -> bits 0, 4, 8, 12
+    bad |= __byte_perm(0x67746361u, 0u, sel) ^ (x | 0x20202020u);  // "acgt"[t] vs the byte
+    const uint32_t c = t ^ ((t >> 1) & 0x01010101u);
+    return (c * 0x01041040u) >> 24;                 // c0 | c1 << 2 | c2 << 4 | c3 << 6
 }
 __device__ __forceinline__ bool valid_byte(uint8_t b) {
     uint8_t y = b | 0x20;
@@ -44,14 +44,12 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t *__restrict__ t
             uint4 v[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) v[q] = ld_stream_v4(text + (wb + 32 * q + lane) * 16);
-            uint32_t m = 0xFFFFFFFFu;
+            uint32_t bad = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                m &= valid4(v[q].x) & valid4(v[q].y) & valid4(v[q].z) & valid4(v[q].w);
-                packed[wb + 32 * q + lane] =
-                    pack4(v[q].x) | (pack4(v[q].y) << 8) | (pack4(v[q].z) << 16) | (pack4(v[q].w) << 24);
-            }
-            ok = (m == 0xFFFFFFFFu);
+            for (int q = 0; q < 4; ++q)
+                packed[wb + 32 * q + lane] = pack4(v[q].x, bad) | (pack4(v[q].y, bad) << 8) |
+                                             (pack4(v[q].z, bad) << 16) | (pack4(v[q].w, bad) << 24);
+            ok = (bad == 0);
         } else {
 #pragma unroll 1
             for (int q = 0; q < 4; ++q) {
