@@ -1,0 +1,139 @@
+"""Turn one round's gpurun_out/ captures into committed evidence under profiles/.
+
+usage: python scripts/make_profile_summary.py <tag> [<round>]
+  reads  gpurun_out/launches_<tag>.csv, gpurun_out/{pack,match,compact}_kernel_<tag>.ncu-rep,
+         gpurun_out/bench_<tag>.json
+  writes profiles/<round>_launches.csv  (ncu gpu__time_duration.sum launch list)
+         profiles/<round>_ncu_summary.md (per-kernel metrics, shares of the step, roofline)
+         profiles/ncu_traffic.json       (dram bytes per launch, read by bench.py)
+"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+KERNELS = ["pack_kernel", "match_kernel", "compact_kernel"]
+ALG = {"pack_kernel": 1.25, "match_kernel": 4.25, "compact_kernel": 4.0}
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads / warp instr"),
+    ("smsp__warps_eligible.avg.per_cycle_active", "eligible warps / scheduler"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smem load wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem load bank conflicts"),
+    ("launch__registers_per_thread", "registers / thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+]
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
+              "nsecond": 1e-9, "second": 1}
+
+
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    return dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+
+
+def val(d, u, k):
+    try:
+        return float(d[k]) * UNIT_SCALE.get(u.get(k, ""), 1)
+    except (KeyError, ValueError):
+        return None
+
+
+def main(tag, rnd="r01"):
+    os.makedirs(PROF, exist_ok=True)
+    bench = None
+    bp = os.path.join(OUT, f"bench_{tag}.json")
+    if os.path.exists(bp):
+        for line in open(bp):
+            if line.startswith("{"):
+                bench = json.loads(line)
+    n = bench["config"]["n_bases_per_rank"] if bench else 256_000_000
+    lines = [f"# ncu summary — {rnd} (tag {tag}), cfg2 (256 Mbp, 1000 x 20-mers), 1x B200", ""]
+    lines.append("Captured with `ncu --set full --clock-control none --import-source on -k regex:<kernel> -s 3 -c 1` "
+                 "around `python bench.py --steps 1 --warmup 3` (scripts/ncu_all.sh). Per-launch times under ncu are "
+                 "cold-cache and serialised; compare shares, not absolutes.")
+    lines.append("")
+    traffic = {}
+    for k in KERNELS:
+        rep = os.path.join(OUT, f"{k}_{tag}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        d, u = raw(rep)
+        lines.append(f"## {k}")
+        lines.append("")
+        lines.append("| metric | value |")
+        lines.append("|---|---|")
+        for key, name in METRICS:
+            if key in d:
+                lines.append(f"| {name} (`{key}`) | {d[key]} {u.get(key, '')} |")
+        rd, wr = val(d, u, "dram__bytes_read.sum"), val(d, u, "dram__bytes_write.sum")
+        dur = val(d, u, "gpu__time_duration.sum")
+        if rd is not None and wr is not None:
+            alg = ALG[k] * n
+            lines.append(f"| DRAM read+write per launch | {(rd + wr) / 1e6:.1f} MB (algorithmic {alg / 1e6:.1f} MB, "
+                         f"ratio {(rd + wr) / alg:.3f}) |")
+            traffic[k.replace("_kernel", "")] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                                                 "algorithmic_bytes": alg, "ncu_duration_s": dur, "n": n}
+        st = {kk: float(vv) for kk, vv in d.items() if kk.startswith("smsp__pcsamp_warps_issue_stalled_")
+              and not kk.endswith("_not_issued") and vv not in ("", "n/a")}
+        tot = sum(st.values()) or 1
+        top = sorted(st.items(), key=lambda x: -x[1])[:6]
+        lines.append("| top stall reasons | " + ", ".join(
+            f"{kk.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * v / tot:.0f}%" for kk, v in top) + " |")
+        lines.append("")
+    # launch list: shares of the step
+    lp = os.path.join(OUT, f"launches_{tag}.csv")
+    if os.path.exists(lp):
+        shutil.copy(lp, os.path.join(PROF, f"{rnd}_launches.csv"))
+        rows = [r for r in csv.reader(open(lp)) if len(r) > 10 and r[0] != "ID"]
+        tot = {}
+        for r in rows:
+            name = r[4]
+            short = next((k for k in KERNELS if k in name), "other: " + name[:40])
+            tot.setdefault(short, []).append(float(r[-1]))
+        lines.append("## Launch list (ncu `gpu__time_duration.sum`, all launches of a 2-step bench run)")
+        lines.append("")
+        lines.append("| kernel | launches | mean ns | share of our kernels' time |")
+        lines.append("|---|---|---|---|")
+        ours = sum(sum(v) for k2, v in tot.items() if k2 in KERNELS)
+        for k2, v in sorted(tot.items()):
+            share = f"{100 * sum(v) / ours:.1f}%" if k2 in KERNELS else "-"
+            lines.append(f"| {k2} | {len(v)} | {sum(v) / len(v):.0f} | {share} |")
+        lines.append("")
+    if bench:
+        kt = bench["kernels_ms"]
+        tot_ms = kt["pack"] + kt["match"] + kt["compact"]
+        lines.append("## Live bench (CUDA events, same build)")
+        lines.append("")
+        lines.append(f"- step {bench['ms_per_step']:.4f} ms → {bench['value']:.1f} Gbases/s; clocks {bench['clocks']}")
+        for k2 in ("pack", "match", "compact"):
+            lines.append(f"- {k2}: {kt[k2]:.4f} ms ({100 * kt[k2] / tot_ms:.1f}% of kernel time)")
+        r = bench["roofline"]
+        lines.append(f"- match roofline: {r['achieved']:.0f} GB/s of {r['peak']} GB/s measured = {r['frac']:.3f}")
+        lines.append("")
+    with open(os.path.join(PROF, f"{rnd}_ncu_summary.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    tp = os.path.join(PROF, "ncu_traffic.json")
+    allt = json.load(open(tp)) if os.path.exists(tp) else {}
+    allt["cfg2"] = traffic
+    allt["cfg2"]["source"] = f"profiles/{rnd}_ncu_summary.md (tag {tag})"
+    json.dump(allt, open(tp, "w"), indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
