@@ -40,14 +40,14 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic(cfg_idx: int):
+def profiled_traffic(cfg_idx: int, path: str):
     """dram bytes per match launch from the committed ncu --set full capture (profiles/), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    e = d.get(f"cfg{cfg_idx}", {}).get("match")
+    e = d.get(f"cfg{cfg_idx}", {}).get("match_fused" if path == "fused" else "match")
     return None if e is None else float(e["dram_bytes_per_launch"])
 
 
@@ -216,7 +216,8 @@ def run_pfac(args):
     bad = torch.zeros(1, dtype=torch.int64, device=dev)
     ws = torch.empty(P.compact_workspace_bytes(n_own), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    kernels_per_step = 3
+    fused = args.path == "fused"
+    kernels_per_step = 2 if fused else 3
 
     def step(ev=None):
         if ev is not None:
@@ -224,12 +225,19 @@ def run_pfac(args):
         P.pack_async(d_text, packed, bad, stream=stream)
         if ev is not None:
             ev[1].record(stream)
-        P.match_packed_async(a, packed, n_own, n_avail, out, stream=stream)
-        if ev is not None:
-            ev[2].record(stream)
-        P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=stream)
-        if ev is not None:
-            ev[3].record(stream)
+        if fused:  # match + compact in one kernel
+            P.match_compact_async(a, packed, n_own, n_avail, out, pos, pid, count, ws, pos_base=sh.start,
+                                  stream=stream)
+            if ev is not None:
+                ev[2].record(stream)
+                ev[3].record(stream)
+        else:
+            P.match_packed_async(a, packed, n_own, n_avail, out, stream=stream)
+            if ev is not None:
+                ev[2].record(stream)
+            P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=stream)
+            if ev is not None:
+                ev[3].record(stream)
         if world > 1:
             m = int(count.item())
             gather_matches(pos, pid, min(m, cap), dst=0)
@@ -268,7 +276,7 @@ def run_pfac(args):
     hbm, hbm_src = peaks()
     pack_ms, match_ms, compact_ms = (float(x) for x in kt.mean(axis=0))
     match_gbs = MATCH_BYTES_PER_BASE * n_own / (match_ms * 1e-3) / 1e9
-    traffic = profiled_traffic(args.config) if args.n is None else None
+    traffic = profiled_traffic(args.config, args.path) if args.n is None else None
 
     # ---- e2e: same step from pinned HOST text, H2D + D2H of the list inside the timed region
     e2e = None
@@ -329,11 +337,15 @@ def run_pfac(args):
                        "l2": "inputs larger than L2 (no flush): ASCII text 1 B/base, out[] 4 B/base",
                        "matches_per_step": m_final},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
-                         "frac": match_gbs / hbm, "traffic": traffic, "kernel": "match",
+                         "frac": match_gbs / hbm, "traffic": traffic,
+                         "kernel": "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel",
                          "algorithmic_bytes_per_launch": MATCH_BYTES_PER_BASE * n_own, "peak_source": hbm_src},
-            "kernels_ms": {"pack": pack_ms, "match": match_ms, "compact": compact_ms,
+            "path": args.path,
+            "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,
+                           "compact": compact_ms,
                            "pack_frac": PACK_BYTES_PER_BASE * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
-                           "compact_frac": COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm},
+                           "compact_frac": (COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm
+                                            if compact_ms > 0 else None)},
             "match_gbases_per_s_per_gpu": n_own / (match_ms * 1e-3) / 1e9,
             "build_ms": build_ms, "prepare_ms": prepare_ms, "gen_s": t_gen,
             "cpu_baseline": cpu, "e2e": e2e,
@@ -354,6 +366,8 @@ def main():
     ap.add_argument("--impl", choices=["pfac", "reference"], default="pfac")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--path", choices=["fused", "separate"], default="fused",
+                    help="fused: pack -> match+compact kernel; separate: pack -> match -> compact")
     ap.add_argument("--n", type=int, default=None, help="override bases per rank (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -123,6 +123,18 @@ int pfac_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *
                  uint32_t *d_pid, uint64_t capacity, uint64_t *count, uint32_t k, uint64_t *d_hist,
                  void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Fused match + compact: one pass that writes out[0..n_own) exactly as
+ * pfac_match_packed_async and the match list exactly as pfac_compact_async(d_out, n_own, pos_base,
+ * ...) would, without re-reading out[].  Same buffer rules as those two calls; d_workspace holds
+ * pfac_compact_workspace_bytes(n_own) bytes; the histogram uses k = pfac_num_patterns(a).
+ * Asynchronous (a cooperative launch: every CTA of the grid is resident at once).
+ */
+int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own,
+                             uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
+                             uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist,
+                             void *d_workspace, void *stream);
+
 /* Thread-local message for the last non-OK return on this thread ("" if none). */
 const char *pfac_last_error(void);
 

@@ -41,6 +41,10 @@ _SIGS = {
     "pfac_compact": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32,
                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_match_compact_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                                ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p]),
     "pfac_last_error": (ctypes.c_char_p, []),
 }
 
@@ -180,6 +184,14 @@ def compact_async(out, pos, pid, count, workspace, pos_base: int = 0, k: int = 0
     """pfac_compact_async into caller buffers (count: 1-element int64 CUDA tensor)."""
     _check(lib().pfac_compact_async(_ptr(out), out.numel(), pos_base, _ptr(pos), _ptr(pid), pos.numel(),
                                     _ptr(count), k, _ptr(hist), _ptr(workspace), _stream(stream, out.device)))
+
+
+def match_compact_async(a: Automaton, packed, n_own: int, n_avail: int, out, pos, pid, count, workspace,
+                        pos_base: int = 0, hist=None, stream=None):
+    """pfac_match_compact_async: fused match + ordered match list (count: 1-element int64 CUDA tensor)."""
+    _check(lib().pfac_match_compact_async(a.handle, _ptr(packed), n_own, n_avail, _ptr(out), pos_base, _ptr(pos),
+                                          _ptr(pid), pos.numel(), _ptr(count), _ptr(hist), _ptr(workspace),
+                                          _stream(stream, out.device)))
 
 
 def compact(out, pos_base: int = 0, capacity: int | None = None, k: int = 0, hist=None, stream=None):

@@ -55,6 +55,7 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     im->S = h.S;
     im->root = h.root;
     im->maxlen = a->maxlen;
+    im->short_pat = h.short_pat;
     im->plan = plan_match(device, h, a->maxlen);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaMalloc(&im->d_J, h.J.size());
@@ -187,6 +188,29 @@ int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32
 }
 
 uint64_t pfac_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
+
+int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
+                             int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                             uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match_compact_async: null automaton");
+    if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_compact_async: n_avail < n_own");
+    if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_match_compact_async: null d_count / d_workspace");
+    if (capacity > 0 && (!d_pos || !d_pid)) return fail(PFAC_E_ARG, "pfac_match_compact_async: null d_pos / d_pid");
+    if (n_own > 0 && (!d_packed || !d_out)) return fail(PFAC_E_ARG, "pfac_match_compact_async: null buffer");
+    if (n_own > 0 && (!aligned16(d_packed) || !aligned16(d_out)))
+        return fail(PFAC_E_ARG, "pfac_match_compact_async: d_packed and d_out must be 16-byte aligned");
+    const int dev = device_of(d_count);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match_compact_async: d_count is not device memory");
+    DeviceImage *im = nullptr;
+    if (n_own > 0) {
+        int rc = get_image(a, dev, &im);
+        if (rc) return rc;
+    }
+    int e = n_own > 0 ? launch_match_compact(*im, a->k, d_packed, n_own, n_avail, d_out, pos_base, d_pos, d_pid,
+                                             capacity, d_count, d_hist, d_workspace, stream)
+                      : cudaMemsetAsync(d_count, 0, 8, (cudaStream_t)stream);
+    return e ? cuda_fail(e, "pfac_match_compact_async") : PFAC_OK;
+}
 
 int pfac_compact_async(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                        uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,

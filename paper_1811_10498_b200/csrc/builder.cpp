@@ -35,7 +35,7 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
     if (k >= 0x7fffffffu) return fail(PFAC_E_TOO_MANY_STATES, "pfac_build: too many patterns");
     char msg[256];
     uint64_t total = 0;
-    uint32_t maxlen = 0;
+    uint32_t maxlen = 0, minlen = 0xFFFFFFFFu;
     // ---- 1. validation, before any allocation that depends on the content
     for (uint32_t j = 0; j < k; ++j) {
         if (offsets[j + 1] < offsets[j]) {
@@ -61,6 +61,7 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
         }
         total += len;
         if (len > maxlen) maxlen = (uint32_t)len;
+        if (len < minlen) minlen = (uint32_t)len;
     }
     // ---- 2. insertion-order trie (a new state per new character)
     std::vector<std::array<uint32_t, 4>> child;
@@ -99,6 +100,7 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
     a->k = k;
     a->S = S;
     a->maxlen = maxlen;
+    a->minlen = k ? minlen : 0;
     try {
         a->table.assign((size_t)S * 4, 0);
         a->depth.assign(S, 0);
@@ -148,6 +150,7 @@ void derive_host_image(pfac_automaton *a) {
     im.cell = (S < 32768u && a->k < 32768u) ? 2 : 4;
     const int K = im.cell == 2 ? kJumpK16 : kJumpK32;
     im.K = K;
+    im.short_pat = a->k > 0 && a->minlen < (uint32_t)K;
     const uint32_t *tab = a->table.data();
     auto nchild = [&](uint32_t u) {
         return (uint32_t)(tab[(size_t)u * 4] != 0) + (tab[(size_t)u * 4 + 1] != 0) + (tab[(size_t)u * 4 + 2] != 0) +

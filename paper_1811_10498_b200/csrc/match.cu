@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "compact_common.cuh"
 #include "pfac_internal.h"
 #include "ptx.cuh"
 
@@ -46,6 +47,9 @@ struct MatchArgs {
     uint32_t window;       // device ids [0, window) have T row / F entry in smem
     uint32_t root;         // device id of the start state
     uint32_t slice_words;  // kSlice/16 + halo words copied per slice (buffers hold +4 words of slack)
+    uint32_t short_pat;    // some pattern is shorter than K: dead J entries may hold nonzero answers
+    uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
+    CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
 };
 
 // One T row (4 cells).  Branch row: child per base.  Chain row: flag|L, then L forced bases.
@@ -138,10 +142,10 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
 constexpr uint32_t kQCap = 128;  // queue of alive positions (drained to < 32 before it could overflow)
 
 static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
-    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2;
+    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + 128;  // + 1024-bit slice match bitmap
 }
 
-template <typename CT, bool WIN, int K>
+template <typename CT, bool WIN, int K, bool FUSE>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
@@ -160,10 +164,18 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint32_t *txt1 = txt0 + p.slice_words + 4;
     uint64_t *bar = reinterpret_cast<uint64_t *>(txt1 + p.slice_words + 4);
     uint16_t *queue = reinterpret_cast<uint16_t *>(bar + 2);
+    uint32_t *bm = reinterpret_cast<uint32_t *>(queue + kQCap);  // fused: nonzero cells of the slice
     const uint32_t lt = (1u << lane) - 1;
+    __shared__ uint64_t s_wcount[kMWarps], s_woff[kMWarps];
 
     const uint64_t TW = (uint64_t)gridDim.x * kMWarps;
     const uint64_t gw = (uint64_t)blockIdx.x * kMWarps + warp;
+    // slice schedule: strided over the grid, or (fused) a contiguous run per warp so that the warp's
+    // matches come out in position order
+    const uint64_t s_first = FUSE ? gw * p.slices_per_warp : gw;
+    const uint64_t s_end = FUSE ? (s_first + p.slices_per_warp < p.nslices ? s_first + p.slices_per_warp : p.nslices)
+                                : p.nslices;
+    const uint64_t s_stride = FUSE ? 1 : TW;
     auto issue = [&](uint64_t sl, uint32_t *dst, uint64_t *b) {
         const uint64_t w0 = sl * (kSlice / 16);
         const uint64_t left = p.avail_words - w0;
@@ -187,14 +199,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             bulk_g2s(sF, p.F, fb, tab_bar);
         }
     }
-    if (lane == 0 && gw < p.nslices) issue(gw, txt0, &bar[0]);
+    if (lane == 0 && s_first < s_end) issue(s_first, txt0, &bar[0]);
     const Tab<CT, WIN> tb{sT, sF, reinterpret_cast<const CT *>(p.T), reinterpret_cast<const CT *>(p.F), p.window};
     mbar_wait(tab_bar, 0);
 
     uint32_t it = 0;
-    for (uint64_t sl = gw; sl < p.nslices; sl += TW, ++it) {
+    uint64_t wcount = 0;  // fused: matches staged by this warp so far
+    uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
+    uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
+    for (uint64_t sl = s_first; sl < s_end; sl += s_stride, ++it) {
         const uint32_t buf = it & 1;
-        if (lane == 0 && sl + TW < p.nslices) issue(sl + TW, buf ? txt0 : txt1, &bar[buf ^ 1]);
+        if (lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
+            if (FUSE) {
+            bm[lane] = 0;
+            __syncwarp();
+        }
         mbar_wait(&bar[buf], (it >> 1) & 1);
         const uint32_t *txt = buf ? txt1 : txt0;
         const uint64_t base = sl * kSlice;
@@ -214,7 +233,9 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 if (lane < take) {
                     const uint32_t l = queue[qn - take + lane];
                     const uint32_t st = (uint32_t)sJ[window16(txt, l) & MASK] & ~ALIVE;
-                    out[l] = (int32_t)walk(tb, txt, st, l + K, lend);
+                    const uint32_t res = walk(tb, txt, st, l + K, lend);
+                    out[l] = (int32_t)res;
+                    if (FUSE && res) atomicOr(&bm[l >> 5], 1u << (l & 31));
                 }
                 qn -= take;
                 __syncwarp();
@@ -251,6 +272,12 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 }
                 st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);  // alive cells are patched by drain()
                 st_stream_v4(out + l0 + 4, e[4], e[5], e[6], e[7]);
+                if (FUSE && p.short_pat) {  // dead walks with an answer (a pattern shorter than K)
+                    uint32_t nz = 0;
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j) nz |= (e[j] != 0 && !(e[j] & ALIVE)) ? (1u << j) : 0u;
+                    if (nz) atomicOr(&bm[l0 >> 5], nz << (l0 & 31));
+                }
             }
             push(am);
         } else {
@@ -282,11 +309,51 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         if (l0 + j < lown) out[l0 + j] = (int32_t)e[j];
                     alive &= (1u << (lown - l0)) - 1;
                 }
+                if (FUSE) {
+                    uint32_t nz = 0;
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j)
+                        nz |= (l0 + j < lown && e[j] != 0 && !(e[j] & ALIVE)) ? (1u << j) : 0u;
+                    if (nz) atomicOr(&bm[l0 >> 5], nz << (l0 & 31));
+                }
                 am |= alive << (r * kP);
             }
             push(am);
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
+        if (FUSE) {  // stage this slice's matches in position order (lane l owns positions 32l..32l+31)
+            uint32_t w = bm[lane];
+            const uint32_t c = __popc(w);
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(~0u, incl, d);
+                if (lane >= (uint32_t)d) incl += y;
+            }
+            uint64_t r = wcount + incl - c;
+            while (w) {
+                const uint32_t bit = __ffs(w) - 1;
+                w &= w - 1;
+                const uint32_t l = lane * 32 + bit;
+                if (r < p.c.stg) {
+                    spos[r] = p.c.pos_base + base + l;
+                    spid[r] = ld_cg_u32(out + l);  // written by this warp before the __syncwarp above
+                }
+                ++r;
+            }
+            wcount += __shfl_sync(~0u, incl, 31);
+        }
+    }
+    if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
+        const uint64_t prefix = grid_prefix<kMWarps>(wcount, p.c.counts, p.c.d_count, s_wcount, s_woff);
+        if (wcount <= p.c.stg) {
+            for (uint64_t i = lane; i < wcount; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);
+        } else {  // staging overflowed (dense matches): re-read this warp's own cells of out[]
+            const uint64_t lo = s_first * kSlice < p.n_own ? s_first * kSlice : p.n_own;
+            const uint64_t hi = s_end * kSlice < p.n_own ? s_end * kSlice : p.n_own;
+            warp_stream(p.c, lo, hi, prefix,
+                        [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); });
+        }
     }
 }
 
@@ -328,10 +395,8 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     return pl;
 }
 
-int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
-                 int32_t *d_out, void *stream) {
-    if (n_own == 0) return cudaSuccess;
-    MatchArgs a;
+static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own,
+                      uint64_t n_avail, int32_t *d_out) {
     a.packed = d_packed;
     a.out = d_out;
     a.n_own = n_own;
@@ -344,18 +409,71 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_ow
     a.window = img.plan.window;
     a.root = img.root;
     a.slice_words = img.plan.slice_words;
+    a.short_pat = img.short_pat;
+    a.slices_per_warp = 0;
+    a.c = CompactArgs{};
+}
+
+template <bool FUSE>
+static const void *kernel_for(const MatchPlan &pl) {
+    if (pl.cell == 2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE>
+                                         : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE>;
+    return pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32, FUSE>
+                       : (const void *)match_kernel<uint32_t, true, kJumpK32, FUSE>;
+}
+
+int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
+                 int32_t *d_out, void *stream) {
+    if (n_own == 0) return cudaSuccess;
+    MatchArgs a;
+    fill_args(a, img, d_packed, n_own, n_avail, d_out);
     const MatchPlan &pl = img.plan;
     void *args[] = {&a};
-    const void *fn;
-    if (pl.cell == 2) fn = pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16>
-                                       : (const void *)match_kernel<uint16_t, true, kJumpK16>;
-    else fn = pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32>
-                          : (const void *)match_kernel<uint32_t, true, kJumpK32>;
+    const void *fn = kernel_for<false>(pl);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     if (e != cudaSuccess) return e;
     uint64_t grid = (a.nslices + kMWarps - 1) / kMWarps;
     if (grid > (uint64_t)pl.sms) grid = pl.sms;
     e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kMT), args, pl.smem, (cudaStream_t)stream);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+// Fused match + compact: out[] and the ordered match list in one pass.
+int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, uint64_t n_own,
+                         uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                         uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_own == 0) return cudaMemsetAsync(d_count, 0, 8, st);
+    MatchArgs a;
+    fill_args(a, img, d_packed, n_own, n_avail, d_out);
+    const MatchPlan &pl = img.plan;
+    const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
+    const uint64_t warps = grid * kMWarps;
+    a.slices_per_warp = (a.nslices + warps - 1) / warps;
+    CompactArgs &c = a.c;
+    c.out = d_out;
+    c.n = n_own;
+    c.pos_base = pos_base;
+    c.pos = d_pos;
+    c.pid = d_pid;
+    c.cap = capacity;
+    c.d_count = d_count;
+    c.k = k;
+    c.hist = d_hist;
+    c.counts = reinterpret_cast<uint64_t *>(d_workspace);
+    const uint64_t entries = stage_entries(n_own);
+    c.stg = entries / warps;
+    c.stage_pos = c.counts + kGMax;
+    c.stage_pid = reinterpret_cast<uint32_t *>(c.stage_pos + entries);
+    c.chunk = a.slices_per_warp * kSlice;
+    cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
+    if (e != cudaSuccess) return e;
+    const void *fn = kernel_for<true>(pl);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    if (e != cudaSuccess) return e;
+    void *args[] = {&a};
+    e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kMT), args, pl.smem, st);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -38,6 +38,7 @@ struct HostImage {
     uint32_t S = 0;                    // device ids 1..S, row 0 is an all-zero dummy
     uint32_t root = 0;                 // device id of the root (= 1)
     uint32_t rows = 0;                 // rows allocated (S + 1 padded to a multiple of 8)
+    uint32_t short_pat = 0;            // a pattern shorter than K exists (dead J cells may be nonzero)
     std::vector<uint8_t> J, T, F;      // raw little-endian cells
 };
 
@@ -57,6 +58,7 @@ struct DeviceImage {
     int K = kJumpK32;
     uint32_t S = 0, root = 0;
     uint32_t maxlen = 0;
+    uint32_t short_pat = 0;
     MatchPlan plan;
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
 };
@@ -67,6 +69,7 @@ struct pfac_automaton {
     uint32_t k = 0;       // patterns
     uint32_t S = 0;       // canonical states (incl. root)
     uint32_t maxlen = 0;
+    uint32_t minlen = 0;
     std::vector<uint32_t> table;  // canonical S*4, columns A,C,G,T
     std::vector<uint32_t> depth;  // canonical depth of each state
     std::vector<uint32_t> F;      // canonical: deepest final on the root path (pattern id) or 0
@@ -92,5 +95,8 @@ int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t
                    uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,
                    void *stream);
 uint64_t compact_workspace_bytes(uint64_t n);
+int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, uint64_t n_own,
+                         uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                         uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 }  // namespace pfac

@@ -112,8 +112,11 @@ def random_patterns(seed: int, k: int, lo: int, hi: int, avoid=None, name: str =
     key = name + ":bases"
     cursor = 0
     buf = iid_text_named(seed, key, 0, need)
+    len_key = substream_key(seed, name + ":relen")
+    redraws = 0
     for j in range(k):
         L = int(lens[j])
+        tries = 0
         while True:
             if cursor + L > len(buf):
                 buf = np.concatenate([buf, iid_text_named(seed, key, len(buf), len(buf) + need)])
@@ -121,6 +124,13 @@ def random_patterns(seed: int, k: int, lo: int, hi: int, avoid=None, name: str =
             cursor += L
             if p not in seen:
                 break
+            tries += 1
+            if tries >= 64:  # this length class may be exhausted (e.g. only 4 patterns of length 1)
+                L = lo + int(u64(len_key, redraws, 1)[0] % np.uint64(hi - lo + 1))
+                redraws += 1
+                tries = 0
+                if redraws > 64 * k + 1024:
+                    raise ValueError(f"cannot draw {k} distinct patterns with lengths in [{lo}, {hi}]")
         seen.add(p)
         pats.append(p)
     return pats

@@ -42,3 +42,12 @@ def test_config_shapes():
     # low complexity: a large fraction of positions sit inside runs
     same = (t5[1:] == t5[:-1]).mean()
     assert same > 0.3
+
+
+def test_exhausted_length_classes_terminate():
+    """Only 4 patterns of length 1 exist: redraw the length instead of looping forever."""
+    P = gen.random_patterns(41, 300, 1, 12)
+    assert len(P) == len(set(P)) == 300 and all(1 <= len(p) <= 12 for p in P)
+    import pytest
+    with pytest.raises(ValueError):
+        gen.random_patterns(1, 30, 1, 2)  # only 4 + 16 = 20 distinct patterns exist

@@ -277,3 +277,68 @@ def test_config5_full():
 @pytest.mark.parametrize("idx", [3, 4])
 def test_config3_config4_full(idx):
     _full_config(idx)
+
+
+# --------------------------------------------------------------------------- fused match + compact
+def _fused(a, text, n_own=None, n_avail=None, pos_base=0, cap=None, k=0, hist=None):
+    n = len(text)
+    n_own = n if n_own is None else n_own
+    n_avail = n if n_avail is None else n_avail
+    packed = P.pack_async(to_dev(text))
+    out = torch.empty(max(n_own, 1), dtype=torch.int32, device=DEV)
+    cap = n_own + 16 if cap is None else cap
+    pos = torch.empty(max(cap, 1), dtype=torch.int64, device=DEV)
+    pid = torch.empty(max(cap, 1), dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ws = torch.empty(P.compact_workspace_bytes(n_own), dtype=torch.uint8, device=DEV)
+    P.binding.match_compact_async(a, packed, n_own, n_avail, out, pos[:cap] if cap else pos[:0], pid[:cap] if cap else pid[:0],
+                                  cnt, ws, pos_base=pos_base, hist=hist)
+    torch.cuda.synchronize()
+    m = int(cnt.item())
+    return out[:n_own].cpu().numpy(), pos[:min(m, cap)].cpu().numpy(), pid[:min(m, cap)].cpu().numpy(), m
+
+
+@pytest.mark.parametrize("case", ["cfg1", "short", "kmers8", "shard", "edge"])
+def test_fused_match_compact(case):
+    if case == "cfg1":
+        cfg = gen.CONFIGS[1]
+        pats = gen.config_patterns(cfg)
+        text = gen.config_text(cfg, patterns=pats)
+        kw = {}
+    elif case == "short":  # patterns shorter than K: dead jump-table cells carry answers
+        pats = gen.random_patterns(41, 300, 1, 12)
+        n = 50 * 1024 + 77
+        text = gen.plant(gen.iid_text(41, 0, n), 0, n, pats, 41)
+        kw = {}
+    elif case == "kmers8":  # every position matches: staging overflows, warps re-read out[]
+        pats = gen.all_kmers(4)
+        text = gen.iid_text(42, 0, 700_001)
+        kw = {}
+    elif case == "shard":
+        pats = gen.random_patterns(43, 200, 5, 40)
+        n = 200_000
+        text = gen.plant(gen.iid_text(43, 0, n), 0, n, pats, 43)
+        kw = dict(n_own=150_003, n_avail=150_003 + 39, pos_base=10_000_000)
+    else:
+        pats = gen.random_patterns(44, 60, 1, 12) + [b"ACGTACGTACGTACGTACGTAC"]
+        text = gen.plant(gen.iid_text(44, 0, 1000), 0, 1000, pats, 44)
+        kw = {}
+    a = P.Automaton(pats)
+    hist = torch.zeros(len(pats) + 1, dtype=torch.int64, device=DEV)
+    out, pos, pid, m = _fused(a, text, hist=hist, **kw)
+    o = Oracle(pats)
+    n_own, n_avail = kw.get("n_own", len(text)), kw.get("n_avail", len(text))
+    exp = o.match(text, 0, n_own, n=n_avail)
+    assert (out == exp).all()
+    epos, epid = o.match_list(text, 0, n_own, n=n_avail)
+    assert m == len(epos)
+    assert (pos == epos.astype(np.int64) + kw.get("pos_base", 0)).all() and (pid == epid).all()
+    assert (hist.cpu().numpy() == np.bincount(epid, minlength=len(pats) + 1)).all()
+
+
+def test_fused_capacity_reports_total():
+    pats = gen.all_kmers(3)
+    text = gen.iid_text(45, 0, 100_000)
+    out, pos, pid, m = _fused(P.Automaton(pats), text, cap=1000)
+    assert m == 100_000 - 2 and len(pos) == 1000
+    assert (pos == np.arange(1000)).all()
