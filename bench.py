@@ -275,6 +275,8 @@ def run_pfac(args):
 
     hbm, hbm_src = peaks()
     pack_ms, match_ms, compact_ms = (float(x) for x in kt.mean(axis=0))
+    if fused:
+        compact_ms = 0.0  # inside the fused kernel
     match_gbs = MATCH_BYTES_PER_BASE * n_own / (match_ms * 1e-3) / 1e9
     traffic = profiled_traffic(args.config, args.path) if args.n is None else None
 
@@ -342,7 +344,7 @@ def run_pfac(args):
                          "algorithmic_bytes_per_launch": MATCH_BYTES_PER_BASE * n_own, "peak_source": hbm_src},
             "path": args.path,
             "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,
-                           "compact": compact_ms,
+                           "compact": None if fused else compact_ms,
                            "pack_frac": PACK_BYTES_PER_BASE * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
                            "compact_frac": (COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm
                                             if compact_ms > 0 else None)},

@@ -375,6 +375,8 @@ static void dev_props(int device, int &sms, int &optin) {
     optin = o;
 }
 
+constexpr size_t kStaticSmemReserve = 1024;  // the fused kernel's static shared arrays (grid_prefix)
+
 static size_t match_smem(int K, uint32_t cell, uint32_t window, uint32_t slice_words) {
     return ((size_t)1 << (2 * K)) * cell + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words) + 16;
 }
@@ -385,7 +387,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     dev_props(device, sms, optin);
     pl.cell = h.cell;
     pl.slice_words = kSlice / 16 + halo_words_for(h.K, maxlen);
-    const size_t fixed = match_smem(h.K, pl.cell, 0, pl.slice_words);
+    const size_t fixed = match_smem(h.K, pl.cell, 0, pl.slice_words) + kStaticSmemReserve;
     const size_t budget = (size_t)optin > fixed ? (size_t)optin - fixed : 0;
     const uint32_t w = (uint32_t)(budget / (5 * pl.cell)) & ~7u;
     pl.all_smem = w >= h.rows;
