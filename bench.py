@@ -209,12 +209,17 @@ def run_pfac(args):
     d_text = h_text.to(dev)
     packed = torch.empty(P.packed_words(n_avail), dtype=torch.int32, device=dev)
     out = torch.empty(n_own, dtype=torch.int32, device=dev)
-    cap = n_own // 1024 + 65536
-    pos = torch.empty(cap, dtype=torch.int64, device=dev)
-    pid = torch.empty(cap, dtype=torch.int32, device=dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
     bad = torch.zeros(1, dtype=torch.int64, device=dev)
     ws = torch.empty(P.compact_workspace_bytes(n_own), dtype=torch.uint8, device=dev)
+    # size the list from a probe pass (the count is exact even when the capacity is exceeded)
+    pos = torch.empty(1, dtype=torch.int64, device=dev)
+    pid = torch.empty(1, dtype=torch.int32, device=dev)
+    P.pack_async(d_text, packed, bad)
+    P.match_compact_async(a, packed, n_own, n_avail, out, pos[:0], pid[:0], count, ws, pos_base=sh.start)
+    cap = int(count.item()) + 1024
+    pos = torch.empty(cap, dtype=torch.int64, device=dev)
+    pid = torch.empty(cap, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     fused = args.path == "fused"
     kernels_per_step = 2 if fused else 3
@@ -284,7 +289,7 @@ def run_pfac(args):
     e2e = None
     if not args.no_e2e:
         e_steps = max(1, min(args.steps, args.e2e_steps))
-        h_pos = torch.empty(cap, dtype=torch.int64).pin_memory()
+        h_pos = torch.empty(cap, dtype=torch.int64).pin_memory()  # cap = measured count + 1024
         h_pid = torch.empty(cap, dtype=torch.int32).pin_memory()
         h_cnt = torch.empty(1, dtype=torch.int64).pin_memory()
         d2h = 0
