@@ -342,7 +342,7 @@ def run_pfac(args):
                        "patterns": len(pats), "states": a.num_states, "max_len": a.max_len,
                        "parallelism": f"text-sharded x{world} (halo maxlen-1)",
                        "l2": "inputs larger than L2 (no flush): ASCII text 1 B/base, out[] 4 B/base",
-                       "matches_per_step": m_final},
+                       "matches_per_step": m_final, "image": a.image_info(local)},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
                          "kernel": "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel",

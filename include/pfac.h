@@ -135,6 +135,22 @@ int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, 
                              uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist,
                              void *d_workspace, void *stream);
 
+/* Device image facts for reports and tests; builds the image if needed. */
+typedef struct {
+    int32_t device;
+    uint32_t cell_bytes;      /* 2 (uint16 image) or 4 */
+    uint32_t K;               /* jump-table length (J has 4^K cells, in shared memory) */
+    uint32_t K2;              /* second-level jump length (0 = none; J2 in L2-persisting memory) */
+    uint32_t states;          /* S */
+    uint32_t window_rows;     /* device states whose row is staged in shared memory */
+    uint32_t all_smem;        /* 1 if every row fits */
+    uint32_t short_pat;       /* a pattern shorter than the jump length exists */
+    uint64_t smem_bytes;      /* dynamic shared memory per CTA of the match kernel */
+    uint64_t l2_persist_bytes;/* access-policy window over J2 */
+    uint64_t image_bytes;     /* device memory of the image */
+} pfac_image_info_t;
+int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out);
+
 /* Thread-local message for the last non-OK return on this thread ("" if none). */
 const char *pfac_last_error(void);
 

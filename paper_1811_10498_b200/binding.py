@@ -45,6 +45,7 @@ _SIGS = {
                                                 ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_void_p]),
+    "pfac_image_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "pfac_last_error": (ctypes.c_char_p, []),
 }
 
@@ -63,6 +64,13 @@ def lib() -> ctypes.CDLL:
             f.argtypes = args
         _lib = L
     return _lib
+
+
+class ImageInfo(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("cell_bytes", ctypes.c_uint32), ("K", ctypes.c_uint32),
+                ("K2", ctypes.c_uint32), ("states", ctypes.c_uint32), ("window_rows", ctypes.c_uint32),
+                ("all_smem", ctypes.c_uint32), ("short_pat", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint64),
+                ("l2_persist_bytes", ctypes.c_uint64), ("image_bytes", ctypes.c_uint64)]
 
 
 class PfacError(RuntimeError):
@@ -138,6 +146,12 @@ class Automaton:
 
     def prepare(self, device: int = 0) -> None:
         _check(lib().pfac_prepare(self._h, device))
+
+    def image_info(self, device: int = 0) -> dict:
+        """pfac_image_info: the device image's layout facts (builds the image if needed)."""
+        info = ImageInfo()
+        _check(lib().pfac_image_info(self._h, device, ctypes.byref(info)))
+        return {name: getattr(info, name) for name, _ in ImageInfo._fields_}
 
 
 def packed_words(n: int) -> int:

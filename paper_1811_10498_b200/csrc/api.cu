@@ -64,7 +64,28 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
+    im->K2 = h.K2;
+    if (e == cudaSuccess && h.K2) {
+        e = cudaMalloc(&im->d_J2, h.J2.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(im->d_J2, h.J2.data(), h.J2.size() * 4, cudaMemcpyHostToDevice);
+        // reserve a persisting L2 set-aside for J2 (device-wide limit; only grown, never shrunk)
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+        size_t want = h.J2.size() * 4;
+        if (want > (size_t)max_window) want = (size_t)max_window;
+        if (want > (size_t)max_persist) want = (size_t)max_persist;
+        size_t cur = 0;
+        if (e == cudaSuccess && want > 0 && cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {
+            if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+                cudaGetLastError();
+                want = cur;
+            }
+            im->l2_persist_bytes = want;
+        }
+    }
     if (e != cudaSuccess) {
+        cudaFree(im->d_J2);
         cudaFree(im->d_J);
         cudaFree(im->d_T);
         cudaFree(im->d_F);
@@ -98,6 +119,7 @@ void pfac_free(pfac_automaton *a) {
         cudaFree(im->d_J);
         cudaFree(im->d_T);
         cudaFree(im->d_F);
+        cudaFree(im->d_J2);
         cudaSetDevice(prev);
         delete im;
     }
@@ -253,6 +275,26 @@ int pfac_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *
                  (unsigned long long)capacity);
         return fail(PFAC_E_CAPACITY, msg);
     }
+    return PFAC_OK;
+}
+
+int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out) {
+    if (!a || !out) return fail(PFAC_E_ARG, "pfac_image_info: null argument");
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, device, &im);
+    if (rc) return rc;
+    const HostImage &h = a->host_image;
+    out->device = device;
+    out->cell_bytes = im->plan.cell;
+    out->K = (uint32_t)im->K;
+    out->K2 = (uint32_t)im->K2;
+    out->states = im->S;
+    out->window_rows = im->plan.window;
+    out->all_smem = im->plan.all_smem ? 1u : 0u;
+    out->short_pat = im->short_pat;
+    out->smem_bytes = im->plan.smem;
+    out->l2_persist_bytes = im->l2_persist_bytes;
+    out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4;
     return PFAC_OK;
 }
 

@@ -150,7 +150,7 @@ void derive_host_image(pfac_automaton *a) {
     im.cell = (S < 32768u && a->k < 32768u) ? 2 : 4;
     const int K = im.cell == 2 ? kJumpK16 : kJumpK32;
     im.K = K;
-    im.short_pat = a->k > 0 && a->minlen < (uint32_t)K;
+    im.short_pat = 0;  // set below, once K2 is known
     const uint32_t *tab = a->table.data();
     auto nchild = [&](uint32_t u) {
         return (uint32_t)(tab[(size_t)u * 4] != 0) + (tab[(size_t)u * 4 + 1] != 0) + (tab[(size_t)u * 4 + 2] != 0) +
@@ -174,11 +174,28 @@ void derive_host_image(pfac_automaton *a) {
                     q.push_back(v);
                 }
     }
+    // Second-level jump table for uint32 images (large automata): K2 in [9, 11] (J2 <= 16 MiB, so it
+    // stays L2-resident next to the out[] stream), the smallest K2 whose depth-K2 states cover <= 3%
+    // of all K2-mers, i.e. <= ~3% of positions still walk after the J2 lookup.
+    im.K2 = 0;
+    if (im.cell == 4) {
+        std::vector<uint64_t> per_depth(a->maxlen + 2, 0);
+        for (uint32_t u = 0; u < S; ++u) per_depth[depth[u]]++;
+        im.K2 = 11;
+        for (int k2 = 9; k2 <= 11; ++k2) {
+            const uint64_t D = (uint32_t)k2 < per_depth.size() ? per_depth[k2] : 0;
+            if (D * 100 <= 3 * (1ull << (2 * k2))) {
+                im.K2 = k2;
+                break;
+            }
+        }
+    }
+    im.short_pat = a->k > 0 && a->minlen < (uint32_t)(im.K2 ? im.K2 : K);
     // Deep-first, chain-major numbering.  Part A: the states at depth >= K, breadth-first over chain
     // heads starting from the depth-K states (the states J hands to the kernel), each head followed
     // by its unary run.  Part B: the states at depth < K, the same way from the root, with runs cut
     // at depth K-1.  Runs never cross the boundary, so every chain row spans consecutive ids.
-    const uint32_t Kd = (uint32_t)K;
+    const uint32_t Kd = (uint32_t)(im.K2 ? im.K2 : K);  // walks resume at depth K2 when J2 exists
     auto unary_next = [&](uint32_t u, uint32_t &v) {  // the only child of u, if u is unary and in u's part
         uint32_t c;
         if (nchild(u) != 1) return false;
@@ -271,6 +288,20 @@ void derive_host_image(pfac_automaton *a) {
             s = t;
         }
         putc(im.J, x, (d == K) ? (alive | dev[s]) : a->F[s]);
+    }
+    if (im.K2) {
+        const uint32_t K2 = (uint32_t)im.K2;
+        const uint64_t n2 = 1ull << (2 * K2);
+        im.J2.assign(n2, 0);
+        for (uint64_t x = 0; x < n2; ++x) {
+            uint32_t s2 = 0, d = 0;
+            for (; d < K2; ++d) {
+                const uint32_t t = tab[(size_t)s2 * 4 + ((x >> (2 * d)) & 3)];
+                if (!t) break;
+                s2 = t;
+            }
+            im.J2[x] = (d == K2) ? (0x80000000u | dev[s2]) : a->F[s2];
+        }
     }
 }
 

@@ -47,7 +47,9 @@ struct MatchArgs {
     uint32_t window;       // device ids [0, window) have T row / F entry in smem
     uint32_t root;         // device id of the start state
     uint32_t slice_words;  // kSlice/16 + halo words copied per slice (buffers hold +4 words of slack)
-    uint32_t short_pat;    // some pattern is shorter than K: dead J entries may hold nonzero answers
+    uint32_t short_pat;    // some pattern is shorter than K (K2): dead J (J2) entries may hold answers
+    const uint32_t *J2;    // second-level jump table (uint32 images), L2-persisting
+    uint32_t K2, mask2;
     uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
     CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
 };
@@ -145,7 +147,7 @@ static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
     return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + 128;  // + 1024-bit slice match bitmap
 }
 
-template <typename CT, bool WIN, int K, bool FUSE>
+template <typename CT, bool WIN, int K, bool FUSE, bool J2M>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
@@ -232,8 +234,14 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 const uint32_t take = qn - keep < 32 ? qn - keep : 32;
                 if (lane < take) {
                     const uint32_t l = queue[qn - take + lane];
-                    const uint32_t st = (uint32_t)sJ[window16(txt, l) & MASK] & ~ALIVE;
-                    const uint32_t res = walk(tb, txt, st, l + K, lend);
+                    const uint32_t x = window16(txt, l);
+                    uint32_t res;
+                    if (J2M && l + p.K2 <= lend) {  // resume at depth K2 (the position is alive there)
+                        const uint32_t g = __ldg(p.J2 + (x & p.mask2));
+                        res = (g & 0x80000000u) ? walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, lend) : g;
+                    } else {
+                        res = walk(tb, txt, (uint32_t)sJ[x & MASK] & ~ALIVE, l + K, lend);
+                    }
                     out[l] = (int32_t)res;
                     if (FUSE && res) atomicOr(&bm[l >> 5], 1u << (l & 31));
                 }
@@ -257,18 +265,45 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
             drain(0);
         };
-        if (lown == kSlice && lend >= kSlice + kP - 1 + K) {
-            // interior slice: every position owned, every K-mer readable
+        if (lown == kSlice && lend >= kSlice + kP - 1 + (J2M ? 16 : K)) {
+            // interior slice: every position owned, every K-mer (K2-mer) readable
             uint32_t am = 0;
+            uint32_t ge[kP], gn[kP];  // J2-mode pipeline registers (current / next sub-slice)
+            auto stage_j2 = [&](uint32_t rr, uint32_t (&g)[kP]) {
+                const uint32_t m0 = rr * kSubN + lane * kP;
+                const uint32_t q = m0 >> 4;
+                const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> ((m0 & 15) * 2);
+                const uint32_t x = (uint32_t)x64;
+#pragma unroll
+                for (uint32_t j = 0; j < kP; ++j) {
+                    const uint32_t e1 = sJ[(x >> (2 * j)) & MASK];
+                    g[j] = (e1 & ALIVE) ? __ldg(p.J2 + ((uint32_t)(x64 >> (2 * j)) & p.mask2)) : e1;
+                }
+            };
+            (void)stage_j2;
 #pragma unroll kPh1Unroll
             for (uint32_t r = 0; r < kSub; ++r) {
                 const uint32_t l0 = r * kSubN + lane * kP;
-                const uint32_t x = window16(txt, l0);
                 uint32_t e[kP];
+                if constexpr (J2M) {
+                    // J answers the walks that die within K bases; every other one is resolved by its
+                    // K2-mer in the L2-resident J2.  Two-stage pipeline over the sub-slices: the J2 loads
+                    // of sub-slice r+1 are in flight while sub-slice r is consumed (up to 16 per lane).
+                    if (r == 0) stage_j2(0, ge);
+                    if (r + 1 < kSub) stage_j2(r + 1, gn);
 #pragma unroll
-                for (uint32_t j = 0; j < kP; ++j) {
-                    e[j] = sJ[(x >> (2 * j)) & MASK];
-                    am |= (e[j] & ALIVE) ? (1u << (r * kP + j)) : 0u;
+                    for (uint32_t j = 0; j < kP; ++j) {
+                        e[j] = ge[j];
+                        am |= (ge[j] & ALIVE) ? (1u << (r * kP + j)) : 0u;
+                        ge[j] = gn[j];
+                    }
+                } else {
+                    const uint32_t x = window16(txt, l0);
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j) {
+                        e[j] = sJ[(x >> (2 * j)) & MASK];
+                        am |= (e[j] & ALIVE) ? (1u << (r * kP + j)) : 0u;
+                    }
                 }
                 st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);  // alive cells are patched by drain()
                 st_stream_v4(out + l0 + 4, e[4], e[5], e[6], e[7]);
@@ -412,16 +447,58 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.root = img.root;
     a.slice_words = img.plan.slice_words;
     a.short_pat = img.short_pat;
+    a.J2 = img.d_J2;
+    a.K2 = (uint32_t)img.K2;
+    a.mask2 = img.K2 ? (uint32_t)((1ull << (2 * img.K2)) - 1) : 0u;
     a.slices_per_warp = 0;
     a.c = CompactArgs{};
 }
 
 template <bool FUSE>
-static const void *kernel_for(const MatchPlan &pl) {
-    if (pl.cell == 2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE>
-                                         : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE>;
-    return pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32, FUSE>
-                       : (const void *)match_kernel<uint32_t, true, kJumpK32, FUSE>;
+static const void *kernel_for(const DeviceImage &img) {
+    const MatchPlan &pl = img.plan;
+    if (pl.cell == 2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, false>
+                                         : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE, false>;
+    if (img.K2) return pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32, FUSE, true>
+                                   : (const void *)match_kernel<uint32_t, true, kJumpK32, FUSE, true>;
+    return pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32, FUSE, false>
+                       : (const void *)match_kernel<uint32_t, true, kJumpK32, FUSE, false>;
+}
+
+// Launch with the image's L2 access-policy window (J2 persisting in L2) and, for the fused kernel,
+// as a cooperative launch (every CTA resident: the grid-wide prefix spins on its predecessors).
+static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchArgs &a, bool cooperative,
+                  cudaStream_t st) {
+    const MatchPlan &pl = img.plan;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kMT);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (cooperative) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    if (img.d_J2 && img.l2_persist_bytes) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = img.d_J2;
+        attr[na].val.accessPolicyWindow.num_bytes = img.l2_persist_bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    void *args[] = {&a};
+    e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
 }
 
 int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
@@ -429,16 +506,9 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_ow
     if (n_own == 0) return cudaSuccess;
     MatchArgs a;
     fill_args(a, img, d_packed, n_own, n_avail, d_out);
-    const MatchPlan &pl = img.plan;
-    void *args[] = {&a};
-    const void *fn = kernel_for<false>(pl);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    if (e != cudaSuccess) return e;
     uint64_t grid = (a.nslices + kMWarps - 1) / kMWarps;
-    if (grid > (uint64_t)pl.sms) grid = pl.sms;
-    e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kMT), args, pl.smem, (cudaStream_t)stream);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (grid > (uint64_t)img.plan.sms) grid = img.plan.sms;
+    return launch(img, kernel_for<false>(img), grid, a, false, (cudaStream_t)stream);
 }
 
 // Fused match + compact: out[] and the ordered match list in one pass.
@@ -471,13 +541,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.chunk = a.slices_per_warp * kSlice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    const void *fn = kernel_for<true>(pl);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    if (e != cudaSuccess) return e;
-    void *args[] = {&a};
-    e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kMT), args, pl.smem, st);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    return launch(img, kernel_for<true>(img), grid, a, true, st);
 }
 
 }  // namespace pfac

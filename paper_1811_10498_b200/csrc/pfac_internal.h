@@ -32,6 +32,9 @@ constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit 
 //  * F[s] = pattern id of the deepest final state on the root path of s (0 = none).
 //  * J[x] for each K-mer x (base t at bits 2t): ALIVE|id of the depth-K state, or F of the deepest
 //    state the K-mer reaches when the walk dies within K bases.
+//  * J2 (uint32 images only): the same over K2-mers, K2 in [9, 12], kept in global memory under an
+//    L2-persisting access-policy window; positions alive after J are resolved by one J2 load, and the
+//    device numbering then starts from the depth-K2 states (where the remaining walks resume).
 struct HostImage {
     int K = kJumpK32;
     uint32_t cell = 4;                 // bytes per cell: 2 if S < 32768 and k < 32768, else 4
@@ -40,6 +43,8 @@ struct HostImage {
     uint32_t rows = 0;                 // rows allocated (S + 1 padded to a multiple of 8)
     uint32_t short_pat = 0;            // a pattern shorter than K exists (dead J cells may be nonzero)
     std::vector<uint8_t> J, T, F;      // raw little-endian cells
+    int K2 = 0;                        // uint32 images: second-level jump over K2-mers (0 = none)
+    std::vector<uint32_t> J2;          // 4^K2 cells, same encoding as J (ALIVE = bit 31); L2-resident
 };
 
 // Launch plan of the match kernel for one automaton on one device (match.cu).
@@ -59,8 +64,11 @@ struct DeviceImage {
     uint32_t S = 0, root = 0;
     uint32_t maxlen = 0;
     uint32_t short_pat = 0;
+    int K2 = 0;
     MatchPlan plan;
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
+    uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
+    size_t l2_persist_bytes = 0;                          // access-policy window over d_J2 (0 = none)
 };
 
 }  // namespace pfac

@@ -358,3 +358,21 @@ def test_fused_capacity_reports_total():
     out, pos, pid, m = _fused(P.Automaton(pats), text, cap=1000)
     assert m == 100_000 - 2 and len(pos) == 1000
     assert (pos == np.arange(1000)).all()
+
+
+# --------------------------------------------------------------------------- large automata (uint32 image + J2)
+@pytest.mark.parametrize("lo,hi,k", [(16, 40, 3000), (8, 30, 5000), (1, 14, 40_000)])
+def test_large_automaton_second_level_jump(lo, hi, k):
+    """uint32 images resolve walks through the L2-resident J2 (K2-mers); short patterns make dead J2
+    cells carry answers (patterns shorter than K2)."""
+    pats = gen.random_patterns(50 + lo, k, lo, hi)
+    n = 300 * 1024 + 555
+    text = gen.plant(gen.iid_text(50 + lo, 0, n), 0, n, pats, 50 + lo)
+    a = P.Automaton(pats)
+    assert a.num_states >= 32768 or k >= 32768  # the uint32 image
+    o = Oracle(pats)
+    assert (gpu_match(a, text) == o.match(text)).all()
+    out, pos, pid, m = _fused(a, text)
+    epos, epid = o.match_list(text)
+    assert (out == o.match(text)).all() and m == len(epos)
+    assert (pos == epos.astype(np.int64)).all() and (pid == epid).all()
