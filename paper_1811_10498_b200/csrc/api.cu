@@ -68,6 +68,8 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     if (e == cudaSuccess && h.K2) {
         e = cudaMalloc(&im->d_J2, h.J2.size() * 4);
         if (e == cudaSuccess) e = cudaMemcpy(im->d_J2, h.J2.data(), h.J2.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&im->d_FB, h.FB.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(im->d_FB, h.FB.data(), h.FB.size() * 4, cudaMemcpyHostToDevice);
         // reserve a persisting L2 set-aside for J2 (device-wide limit; only grown, never shrunk)
         int max_persist = 0, max_window = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
@@ -86,6 +88,7 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     }
     if (e != cudaSuccess) {
         cudaFree(im->d_J2);
+        cudaFree(im->d_FB);
         cudaFree(im->d_J);
         cudaFree(im->d_T);
         cudaFree(im->d_F);
@@ -120,6 +123,7 @@ void pfac_free(pfac_automaton *a) {
         cudaFree(im->d_T);
         cudaFree(im->d_F);
         cudaFree(im->d_J2);
+        cudaFree(im->d_FB);
         cudaSetDevice(prev);
         delete im;
     }
@@ -294,7 +298,7 @@ int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out)
     out->short_pat = im->short_pat;
     out->smem_bytes = im->plan.smem;
     out->l2_persist_bytes = im->l2_persist_bytes;
-    out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4;
+    out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4 + h.FB.size() * 4;
     return PFAC_OK;
 }
 

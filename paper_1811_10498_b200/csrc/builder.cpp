@@ -174,15 +174,15 @@ void derive_host_image(pfac_automaton *a) {
                     q.push_back(v);
                 }
     }
-    // Second-level jump table for uint32 images (large automata): K2 in [9, 11] (J2 <= 16 MiB, so it
-    // stays L2-resident next to the out[] stream), the smallest K2 whose depth-K2 states cover <= 3%
-    // of all K2-mers, i.e. <= ~3% of positions still walk after the J2 lookup.
+    // uint32 images (large automata): a K1-mer filter bitmap (K1 = 10, 128 KiB, in shared memory)
+    // plus a second-level jump table J2 over K2-mers, K2 in [10, 11] (J2 <= 16 MiB, L2-resident next
+    // to the out[] stream): the smallest K2 whose depth-K2 states cover <= 3% of all K2-mers.
     im.K2 = 0;
     if (im.cell == 4) {
         std::vector<uint64_t> per_depth(a->maxlen + 2, 0);
         for (uint32_t u = 0; u < S; ++u) per_depth[depth[u]]++;
         im.K2 = 11;
-        for (int k2 = 9; k2 <= 11; ++k2) {
+        for (int k2 = kFilterK; k2 <= 11; ++k2) {
             const uint64_t D = (uint32_t)k2 < per_depth.size() ? per_depth[k2] : 0;
             if (D * 100 <= 3 * (1ull << (2 * k2))) {
                 im.K2 = k2;
@@ -301,6 +301,20 @@ void derive_host_image(pfac_automaton *a) {
                 s2 = t;
             }
             im.J2[x] = (d == K2) ? (0x80000000u | dev[s2]) : a->F[s2];
+        }
+        // FB[x] = 1 iff the K1-mer x starts a walk that survives K1 bases or completes a pattern on the
+        // way: every other position's answer is 0 without touching J2.
+        const uint32_t K1 = (uint32_t)kFilterK;
+        const uint64_t n1 = 1ull << (2 * K1);
+        im.FB.assign(n1 / 32, 0);
+        for (uint64_t x = 0; x < n1; ++x) {
+            uint32_t s1 = 0, d = 0;
+            for (; d < K1; ++d) {
+                const uint32_t t = tab[(size_t)s1 * 4 + ((x >> (2 * d)) & 3)];
+                if (!t) break;
+                s1 = t;
+            }
+            if (d == K1 || a->F[s1] != 0) im.FB[x >> 5] |= 1u << (x & 31);
         }
     }
 }

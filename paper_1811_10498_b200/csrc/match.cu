@@ -49,6 +49,7 @@ struct MatchArgs {
     uint32_t slice_words;  // kSlice/16 + halo words copied per slice (buffers hold +4 words of slack)
     uint32_t short_pat;    // some pattern is shorter than K (K2): dead J (J2) entries may hold answers
     const uint32_t *J2;    // second-level jump table (uint32 images), L2-persisting
+    const uint32_t *FB;    // uint32 images: the K1-mer filter bitmap (staged in smem instead of J)
     uint32_t K2, mask2;
     uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
     CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
@@ -141,21 +142,25 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
     return tb.final_of(s);
 }
 
-constexpr uint32_t kQCap = 128;  // queue of alive positions (drained to < 32 before it could overflow)
+constexpr uint32_t kQCap = 128;
+constexpr int kFBK = 10;                            // filter length K1 of uint32 images (FBM)
+constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^10 bits = 128 KiB of shared memory  // queue of alive positions (drained to < 32 before it could overflow)
 
 static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
     return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + 128;  // + 1024-bit slice match bitmap
 }
 
-template <typename CT, bool WIN, int K, bool FUSE, bool J2M>
+template <typename CT, bool WIN, int K, bool FUSE, bool FBM>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
     static_assert(kP + K - 1 <= 16, "the eight K-mers of a lane come from one 32-bit window");
+    constexpr uint32_t FBMASK = (1u << (2 * kFBK)) - 1;
     extern __shared__ __align__(128) uint8_t smem[];
-    CT *sJ = reinterpret_cast<CT *>(smem);
-    CT *sT = sJ + NJ;
+    CT *sJ = reinterpret_cast<CT *>(smem);                 // J (4^K cells) ...
+    const uint32_t *sFB = reinterpret_cast<const uint32_t *>(smem);  // ... or, FBM: the K1-mer filter
+    CT *sT = reinterpret_cast<CT *>(smem + (FBM ? kFBBytes : NJ * sizeof(CT)));
     CT *sF = sT + (size_t)p.window * 4;
     uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + p.window);  // 16-byte aligned (W % 8 == 0)
     const uint32_t WB = warp_bytes(p.slice_words);
@@ -193,9 +198,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     fence_mbar_init();
     __syncthreads();
     if (tid == 0) {
-        const uint32_t jb = NJ * sizeof(CT), tb = p.window * 4 * sizeof(CT), fb = p.window * sizeof(CT);
+        const uint32_t jb = FBM ? kFBBytes : NJ * sizeof(CT), tb = p.window * 4 * sizeof(CT),
+                       fb = p.window * sizeof(CT);
         mbar_expect_tx(tab_bar, jb + tb + fb);
-        bulk_g2s(sJ, p.J, jb, tab_bar);
+        bulk_g2s(smem, FBM ? (const void *)p.FB : p.J, jb, tab_bar);
         if (p.window) {
             bulk_g2s(sT, p.T, tb, tab_bar);
             bulk_g2s(sF, p.F, fb, tab_bar);
@@ -236,9 +242,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint32_t l = queue[qn - take + lane];
                     const uint32_t x = window16(txt, l);
                     uint32_t res;
-                    if (J2M && l + p.K2 <= lend) {  // resume at depth K2 (the position is alive there)
-                        const uint32_t g = __ldg(p.J2 + (x & p.mask2));
-                        res = (g & 0x80000000u) ? walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, lend) : g;
+                    if constexpr (FBM) {  // J2 answers the first K2 bases; the rare survivors walk on
+                        if (l + p.K2 <= lend) {
+                            const uint32_t g = __ldg(p.J2 + (x & p.mask2));
+                            res = (g & 0x80000000u) ? walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, lend) : g;
+                        } else {
+                            res = walk(tb, txt, p.root, l, lend);
+                        }
                     } else {
                         res = walk(tb, txt, (uint32_t)sJ[x & MASK] & ~ALIVE, l + K, lend);
                     }
@@ -265,54 +275,55 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
             drain(0);
         };
-        if (lown == kSlice && lend >= kSlice + kP - 1 + (J2M ? 16 : K)) {
-            // interior slice: every position owned, every K-mer (K2-mer) readable
+        if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K)) {
+            // interior slice: every position owned, every K-mer (K1-mer, K2-mer) readable
             uint32_t am = 0;
-            uint32_t ge[kP], gn[kP];  // J2-mode pipeline registers (current / next sub-slice)
-            auto stage_j2 = [&](uint32_t rr, uint32_t (&g)[kP]) {
-                const uint32_t m0 = rr * kSubN + lane * kP;
-                const uint32_t q = m0 >> 4;
-                const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> ((m0 & 15) * 2);
-                const uint32_t x = (uint32_t)x64;
-#pragma unroll
-                for (uint32_t j = 0; j < kP; ++j) {
-                    const uint32_t e1 = sJ[(x >> (2 * j)) & MASK];
-                    g[j] = (e1 & ALIVE) ? __ldg(p.J2 + ((uint32_t)(x64 >> (2 * j)) & p.mask2)) : e1;
-                }
-            };
-            (void)stage_j2;
 #pragma unroll kPh1Unroll
             for (uint32_t r = 0; r < kSub; ++r) {
                 const uint32_t l0 = r * kSubN + lane * kP;
-                uint32_t e[kP];
-                if constexpr (J2M) {
-                    // J answers the walks that die within K bases; every other one is resolved by its
-                    // K2-mer in the L2-resident J2.  Two-stage pipeline over the sub-slices: the J2 loads
-                    // of sub-slice r+1 are in flight while sub-slice r is consumed (up to 16 per lane).
-                    if (r == 0) stage_j2(0, ge);
-                    if (r + 1 < kSub) stage_j2(r + 1, gn);
+                if constexpr (FBM) {
+                    // One filter bit per position: is the K1-mer at l0+j the start of a walk that survives
+                    // K1 bases or completes a pattern?  Almost every answer is 0 and stored right away;
+                    // the flagged positions are queued and resolved by J2 (+ a rare walk) in drain().
+                    const uint32_t q = l0 >> 4;
+                    const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> ((l0 & 15) * 2);
+                    uint32_t m = 0;
 #pragma unroll
                     for (uint32_t j = 0; j < kP; ++j) {
-                        e[j] = ge[j];
-                        am |= (ge[j] & ALIVE) ? (1u << (r * kP + j)) : 0u;
-                        ge[j] = gn[j];
+                        const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
+                        m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
                     }
+                    st_stream_v4(out + l0, 0u, 0u, 0u, 0u);
+                    st_stream_v4(out + l0 + 4, 0u, 0u, 0u, 0u);
+                    am |= m << (r * kP);
                 } else {
+                    uint32_t e[kP];
                     const uint32_t x = window16(txt, l0);
 #pragma unroll
                     for (uint32_t j = 0; j < kP; ++j) {
                         e[j] = sJ[(x >> (2 * j)) & MASK];
                         am |= (e[j] & ALIVE) ? (1u << (r * kP + j)) : 0u;
                     }
-                }
-                st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);  // alive cells are patched by drain()
-                st_stream_v4(out + l0 + 4, e[4], e[5], e[6], e[7]);
-                if (FUSE && p.short_pat) {  // dead walks with an answer (a pattern shorter than K)
-                    uint32_t nz = 0;
+                    st_stream_v4(out + l0, e[0], e[1], e[2], e[3]);  // alive cells are patched by drain()
+                    st_stream_v4(out + l0 + 4, e[4], e[5], e[6], e[7]);
+                    if (FUSE && p.short_pat) {  // dead walks with an answer (a pattern shorter than K)
+                        uint32_t nz = 0;
 #pragma unroll
-                    for (uint32_t j = 0; j < kP; ++j) nz |= (e[j] != 0 && !(e[j] & ALIVE)) ? (1u << j) : 0u;
-                    if (nz) atomicOr(&bm[l0 >> 5], nz << (l0 & 31));
+                        for (uint32_t j = 0; j < kP; ++j)
+                            nz |= (e[j] != 0 && !(e[j] & ALIVE)) ? (1u << j) : 0u;
+                        if (nz) atomicOr(&bm[l0 >> 5], nz << (l0 & 31));
+                    }
                 }
+            }
+            push(am);
+        } else if (FBM) {  // slice at the end of the text: every owned position goes through drain()
+            uint32_t am = 0;
+#pragma unroll 1
+            for (uint32_t r = 0; r < kSub; ++r) {
+                const uint32_t l0 = r * kSubN + lane * kP;
+                if (l0 >= lown) continue;
+                const uint32_t own = lown - l0 >= kP ? 0xFFu : (1u << (lown - l0)) - 1;
+                am |= own << (r * kP);
             }
             push(am);
         } else {
@@ -412,8 +423,8 @@ static void dev_props(int device, int &sms, int &optin) {
 
 constexpr size_t kStaticSmemReserve = 1024;  // the fused kernel's static shared arrays (grid_prefix)
 
-static size_t match_smem(int K, uint32_t cell, uint32_t window, uint32_t slice_words) {
-    return ((size_t)1 << (2 * K)) * cell + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words) + 16;
+static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words) {
+    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words) + 16;
 }
 
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
@@ -421,13 +432,14 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     int sms = 0, optin = 0;
     dev_props(device, sms, optin);
     pl.cell = h.cell;
-    pl.slice_words = kSlice / 16 + halo_words_for(h.K, maxlen);
-    const size_t fixed = match_smem(h.K, pl.cell, 0, pl.slice_words) + kStaticSmemReserve;
+    pl.slice_words = kSlice / 16 + halo_words_for(h.K2 > h.K ? h.K2 : h.K, maxlen);
+    const size_t table = h.K2 ? (size_t)kFBBytes : ((size_t)1 << (2 * h.K)) * pl.cell;
+    const size_t fixed = match_smem(table, pl.cell, 0, pl.slice_words) + kStaticSmemReserve;
     const size_t budget = (size_t)optin > fixed ? (size_t)optin - fixed : 0;
     const uint32_t w = (uint32_t)(budget / (5 * pl.cell)) & ~7u;
     pl.all_smem = w >= h.rows;
     pl.window = pl.all_smem ? h.rows : w;
-    pl.smem = match_smem(h.K, pl.cell, pl.window, pl.slice_words);
+    pl.smem = match_smem(table, pl.cell, pl.window, pl.slice_words);
     pl.sms = sms;
     return pl;
 }
@@ -448,6 +460,7 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.slice_words = img.plan.slice_words;
     a.short_pat = img.short_pat;
     a.J2 = img.d_J2;
+    a.FB = img.d_FB;
     a.K2 = (uint32_t)img.K2;
     a.mask2 = img.K2 ? (uint32_t)((1ull << (2 * img.K2)) - 1) : 0u;
     a.slices_per_warp = 0;

@@ -15,7 +15,8 @@ namespace pfac {
 #define PFAC_K16 8
 #endif
 constexpr int kJumpK16 = PFAC_K16;  // K for uint16 images: J has 4^8 cells = 128 KiB
-constexpr int kJumpK32 = 7;   // K for uint32 images: J has 4^7 cells = 64 KiB
+constexpr int kJumpK32 = 7;   // K for uint32 images: J has 4^7 cells = 64 KiB (edge use only)
+constexpr int kFilterK = 10;  // uint32 images: K1-mer filter bitmap, 4^10 bits = 128 KiB
 constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
 
 // Host-side device image: everything the match kernel reads, already in its cell width.
@@ -32,9 +33,11 @@ constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit 
 //  * F[s] = pattern id of the deepest final state on the root path of s (0 = none).
 //  * J[x] for each K-mer x (base t at bits 2t): ALIVE|id of the depth-K state, or F of the deepest
 //    state the K-mer reaches when the walk dies within K bases.
-//  * J2 (uint32 images only): the same over K2-mers, K2 in [9, 12], kept in global memory under an
-//    L2-persisting access-policy window; positions alive after J are resolved by one J2 load, and the
-//    device numbering then starts from the depth-K2 states (where the remaining walks resume).
+//  * uint32 images (large automata) replace J in shared memory by FB, a 4^10-bit filter: bit x says
+//    whether the 10-mer x starts a walk that survives 10 bases or completes a pattern.  Unflagged
+//    positions answer 0; flagged ones are resolved by J2, the jump table over K2-mers (K2 in
+//    [10, 11]) kept in global memory under an L2-persisting access-policy window, and the rare
+//    survivors walk on from the depth-K2 state; the device numbering then starts at depth K2.
 struct HostImage {
     int K = kJumpK32;
     uint32_t cell = 4;                 // bytes per cell: 2 if S < 32768 and k < 32768, else 4
@@ -45,6 +48,7 @@ struct HostImage {
     std::vector<uint8_t> J, T, F;      // raw little-endian cells
     int K2 = 0;                        // uint32 images: second-level jump over K2-mers (0 = none)
     std::vector<uint32_t> J2;          // 4^K2 cells, same encoding as J (ALIVE = bit 31); L2-resident
+    std::vector<uint32_t> FB;          // K2 > 0: 4^kFilterK-bit filter ("this K1-mer needs J2")
 };
 
 // Launch plan of the match kernel for one automaton on one device (match.cu).
@@ -68,6 +72,7 @@ struct DeviceImage {
     MatchPlan plan;
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
     uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
+    uint32_t *d_FB = nullptr;                             // K2 > 0: K1-mer filter bitmap
     size_t l2_persist_bytes = 0;                          // access-policy window over d_J2 (0 = none)
 };
 
