@@ -178,7 +178,7 @@ void derive_host_image(pfac_automaton *a) {
     // plus a second-level jump table J2 over K2-mers, K2 in [10, 11] (J2 <= 16 MiB, L2-resident next
     // to the out[] stream): the smallest K2 whose depth-K2 states cover <= 3% of all K2-mers.
     im.K2 = 0;
-    if (im.cell == 4) {
+    if (im.cell == 4 || kFilterSmall) {
         std::vector<uint64_t> per_depth(a->maxlen + 2, 0);
         for (uint32_t u = 0; u < S; ++u) per_depth[depth[u]]++;
         im.K2 = 11;

@@ -470,6 +470,8 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
 template <bool FUSE>
 static const void *kernel_for(const DeviceImage &img) {
     const MatchPlan &pl = img.plan;
+    if (pl.cell == 2 && img.K2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, true>
+                                                   : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE, true>;
     if (pl.cell == 2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, false>
                                          : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE, false>;
     if (img.K2) return pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32, FUSE, true>

@@ -17,6 +17,10 @@ namespace pfac {
 constexpr int kJumpK16 = PFAC_K16;  // K for uint16 images: J has 4^8 cells = 128 KiB
 constexpr int kJumpK32 = 7;   // K for uint32 images: J has 4^7 cells = 64 KiB (edge use only)
 constexpr int kFilterK = 10;  // uint32 images: K1-mer filter bitmap, 4^10 bits = 128 KiB
+#ifndef PFAC_FB16
+#define PFAC_FB16 1
+#endif
+constexpr bool kFilterSmall = PFAC_FB16;  // filter + J2 for uint16 images too (A/B knob)
 constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
 
 // Host-side device image: everything the match kernel reads, already in its cell width.
