@@ -18,8 +18,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
-KERNELS = ["pack_kernel", "match_kernel", "compact_kernel"]
-ALG = {"pack_kernel": 1.25, "match_kernel": 4.25, "compact_kernel": 4.0}
+KERNELS = ["pack_kernel", "match_fused", "match_kernel", "compact_kernel"]
+ALG = {"pack_kernel": 1.25, "match_fused": 4.25, "match_kernel": 4.25, "compact_kernel": 4.0}
+TITLES = {"pack_kernel": "pack_kernel", "match_fused": "match_kernel<FUSE=1> (match + compact, bench default)",
+          "match_kernel": "match_kernel<FUSE=0> (--path separate)", "compact_kernel": "compact_kernel (--path separate)"}
+TRAFFIC_KEY = {"pack_kernel": "pack", "match_fused": "match_fused", "match_kernel": "match",
+               "compact_kernel": "compact"}
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "DRAM read"),
@@ -37,7 +41,7 @@ METRICS = [
     ("launch__block_size", "block"),
 ]
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
-              "nsecond": 1e-9, "second": 1}
+              "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}
 
 
 def raw(rep):
@@ -63,6 +67,9 @@ def main(tag, rnd="r01"):
                 bench = json.loads(line)
     n = bench["config"]["n_bases_per_rank"] if bench else 256_000_000
     lines = [f"# ncu summary — {rnd} (tag {tag}), cfg2 (256 Mbp, 1000 x 20-mers), 1x B200", ""]
+    if bench and "image" in bench.get("config", {}):
+        lines.append(f"Device image: {bench['config']['image']}")
+        lines.append("")
     lines.append("Captured with `ncu --set full --clock-control none --import-source on -k regex:<kernel> -s 3 -c 1` "
                  "around `python bench.py --steps 1 --warmup 3` (scripts/ncu_all.sh). Per-launch times under ncu are "
                  "cold-cache and serialised; compare shares, not absolutes.")
@@ -73,7 +80,7 @@ def main(tag, rnd="r01"):
         if not os.path.exists(rep):
             continue
         d, u = raw(rep)
-        lines.append(f"## {k}")
+        lines.append(f"## {TITLES[k]}")
         lines.append("")
         lines.append("| metric | value |")
         lines.append("|---|---|")
@@ -86,7 +93,7 @@ def main(tag, rnd="r01"):
             alg = ALG[k] * n
             lines.append(f"| DRAM read+write per launch | {(rd + wr) / 1e6:.1f} MB (algorithmic {alg / 1e6:.1f} MB, "
                          f"ratio {(rd + wr) / alg:.3f}) |")
-            traffic[k.replace("_kernel", "")] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+            traffic[TRAFFIC_KEY[k]] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                                                  "algorithmic_bytes": alg, "ncu_duration_s": dur, "n": n}
         st = {kk: float(vv) for kk, vv in d.items() if kk.startswith("smsp__pcsamp_warps_issue_stalled_")
               and not kk.endswith("_not_issued") and vv not in ("", "n/a")}
@@ -101,27 +108,29 @@ def main(tag, rnd="r01"):
         shutil.copy(lp, os.path.join(PROF, f"{rnd}_launches.csv"))
         rows = [r for r in csv.reader(open(lp)) if len(r) > 10 and r[0] != "ID"]
         tot = {}
+        names = {"pack_kernel": "pack_kernel", "match_kernel": "match_kernel", "compact_kernel": "compact_kernel"}
         for r in rows:
             name = r[4]
-            short = next((k for k in KERNELS if k in name), "other: " + name[:40])
+            short = next((v for k, v in names.items() if k in name), "other: " + name[:40])
             tot.setdefault(short, []).append(float(r[-1]))
         lines.append("## Launch list (ncu `gpu__time_duration.sum`, all launches of a 2-step bench run)")
         lines.append("")
         lines.append("| kernel | launches | mean ns | share of our kernels' time |")
         lines.append("|---|---|---|---|")
-        ours = sum(sum(v) for k2, v in tot.items() if k2 in KERNELS)
+        ours = sum(sum(v) for k2, v in tot.items() if not k2.startswith("other"))
         for k2, v in sorted(tot.items()):
-            share = f"{100 * sum(v) / ours:.1f}%" if k2 in KERNELS else "-"
+            share = f"{100 * sum(v) / ours:.1f}%" if not k2.startswith("other") else "-"
             lines.append(f"| {k2} | {len(v)} | {sum(v) / len(v):.0f} | {share} |")
         lines.append("")
     if bench:
-        kt = bench["kernels_ms"]
-        tot_ms = kt["pack"] + kt["match"] + kt["compact"]
+        kt = {k2: v for k2, v in bench["kernels_ms"].items() if isinstance(v, float) and not k2.endswith("frac")}
+        tot_ms = sum(kt.values())
         lines.append("## Live bench (CUDA events, same build)")
         lines.append("")
-        lines.append(f"- step {bench['ms_per_step']:.4f} ms → {bench['value']:.1f} Gbases/s; clocks {bench['clocks']}")
-        for k2 in ("pack", "match", "compact"):
-            lines.append(f"- {k2}: {kt[k2]:.4f} ms ({100 * kt[k2] / tot_ms:.1f}% of kernel time)")
+        lines.append(f"- path {bench.get('path')}: step {bench['ms_per_step']:.4f} ms → {bench['value']:.1f} Gbases/s; "
+                     f"clocks {bench['clocks']}")
+        for k2, v in kt.items():
+            lines.append(f"- {k2}: {v:.4f} ms ({100 * v / tot_ms:.1f}% of kernel time)")
         r = bench["roofline"]
         lines.append(f"- match roofline: {r['achieved']:.0f} GB/s of {r['peak']} GB/s measured = {r['frac']:.3f}")
         lines.append("")
