@@ -135,6 +135,21 @@ int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, 
                              uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist,
                              void *d_workspace, void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * End to end over HOST memory (the call a user with a text in RAM makes): the match list
+ * {(pos_base + i, out[i]) : out[i] != 0, i < n_own} of the ASCII text h_text[0..n_avail) (walks
+ * read up to n_avail >= n_own: a shard and its halo) on CUDA device `device`.  The text is streamed
+ * in chunks with a (max_len - 1)-base halo: the host-to-device copy of chunk c+1 runs on one stream
+ * while chunk c is packed and matched + compacted (fused kernel) on another, and each chunk's list
+ * is copied back into h_pos/h_pid at its offset.  Pinned h_text gives copy/compute overlap;
+ * pageable memory works too.  Returns PFAC_E_NON_ACGT (the list is then unspecified) if a byte is
+ * outside ACGTacgt (*first_bad, nullable, receives its index), PFAC_E_CAPACITY if count > capacity
+ * (the first `capacity` entries are written and *count is the total).  Synchronous.
+ */
+int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, uint64_t n_own,
+                   uint64_t n_avail, uint64_t pos_base, uint64_t *h_pos, uint32_t *h_pid,
+                   uint64_t capacity, uint64_t *count, uint64_t *first_bad);
+
 /* Device image facts for reports and tests; builds the image if needed. */
 typedef struct {
     int32_t device;

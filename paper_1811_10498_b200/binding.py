@@ -46,6 +46,9 @@ _SIGS = {
                                                 ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_void_p]),
     "pfac_image_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "pfac_scan_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                      ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_last_error": (ctypes.c_char_p, []),
 }
 
@@ -206,6 +209,36 @@ def match_compact_async(a: Automaton, packed, n_own: int, n_avail: int, out, pos
     _check(lib().pfac_match_compact_async(a.handle, _ptr(packed), n_own, n_avail, _ptr(out), pos_base, _ptr(pos),
                                           _ptr(pid), pos.numel(), _ptr(count), _ptr(hist), _ptr(workspace),
                                           _stream(stream, out.device)))
+
+
+def scan_host(a: Automaton, text, pos=None, pid=None, device: int = 0, n_own: int | None = None,
+              pos_base: int = 0):
+    """pfac_scan_host: the match list of a HOST text (CPU uint8 tensor or numpy array), end to end.
+
+    Positions [0, n_own) are matched (default: all), walks read the whole text (a shard + halo).
+    pos/pid: optional preallocated CPU int64/int32 tensors (pinned for fast copies); the call retries
+    once with exact-size buffers if they are too small.  Returns (pos, pid, count)."""
+    import torch
+    t = torch.as_tensor(text) if not isinstance(text, torch.Tensor) else text
+    assert t.device.type == "cpu" and t.dtype == torch.uint8 and t.is_contiguous()
+    n_avail = t.numel()
+    n = n_avail if n_own is None else n_own
+    if pos is None:
+        cap = n // 64 + 1024
+        pos = torch.empty(cap, dtype=torch.int64)
+        pid = torch.empty(cap, dtype=torch.int32)
+    c = ctypes.c_uint64(0)
+    bad = ctypes.c_uint64(0)
+    rc = lib().pfac_scan_host(a.handle, device, t.data_ptr(), n, n_avail, pos_base, pos.data_ptr(), pid.data_ptr(),
+                              pos.numel(), ctypes.byref(c), ctypes.byref(bad))
+    if rc == E_CAPACITY:
+        pos = torch.empty(int(c.value), dtype=torch.int64)
+        pid = torch.empty(int(c.value), dtype=torch.int32)
+        rc = lib().pfac_scan_host(a.handle, device, t.data_ptr(), n, n_avail, pos_base, pos.data_ptr(),
+                                  pid.data_ptr(), pos.numel(), ctypes.byref(c), ctypes.byref(bad))
+    _check(rc)
+    m = int(c.value)
+    return pos[:m], pid[:m], m
 
 
 def compact(out, pos_base: int = 0, capacity: int | None = None, k: int = 0, hist=None, stream=None):

@@ -124,6 +124,7 @@ void pfac_free(pfac_automaton *a) {
         cudaFree(im->d_F);
         cudaFree(im->d_J2);
         cudaFree(im->d_FB);
+        if (im->scan) free_scan_ctx(im->scan);
         cudaSetDevice(prev);
         delete im;
     }
@@ -276,6 +277,177 @@ int pfac_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *
     if (c > capacity) {
         char msg[128];
         snprintf(msg, sizeof msg, "pfac_compact: %llu matches > capacity %llu", (unsigned long long)c,
+                 (unsigned long long)capacity);
+        return fail(PFAC_E_CAPACITY, msg);
+    }
+    return PFAC_OK;
+}
+
+}  // extern "C"
+
+namespace pfac {
+// Device buffers of one pipeline slot of pfac_scan_host.
+struct ScanSlot {
+    uint8_t *text = nullptr;
+    uint32_t *packed = nullptr;
+    int32_t *out = nullptr;
+    uint64_t *pos = nullptr, *cnt = nullptr, *bad = nullptr;
+    uint32_t *pid = nullptr;
+    void *ws = nullptr;
+    uint64_t cap = 0;
+    cudaEvent_t h2d = nullptr, done = nullptr;
+};
+// pfac_scan_host's pipeline resources, kept with the device image and reused across calls.
+struct ScanCtx {
+    std::mutex mu;
+    uint64_t chunk = 0, halo = 0;
+    cudaStream_t cs = nullptr, xs = nullptr;  // compute, copy
+    ScanSlot slot[2];
+    uint64_t *h_cnt = nullptr;  // pinned: per-slot count and first-bad
+    ~ScanCtx() {
+        for (ScanSlot &sl : slot) {
+            cudaFree(sl.text);
+            cudaFree(sl.packed);
+            cudaFree(sl.out);
+            cudaFree(sl.pos);
+            cudaFree(sl.pid);
+            cudaFree(sl.cnt);
+            cudaFree(sl.ws);
+            if (sl.h2d) cudaEventDestroy(sl.h2d);
+            if (sl.done) cudaEventDestroy(sl.done);
+        }
+        if (h_cnt) cudaFreeHost(h_cnt);
+        if (cs) cudaStreamDestroy(cs);
+        if (xs) cudaStreamDestroy(xs);
+    }
+    cudaError_t init(uint64_t chunk_, uint64_t halo_) {
+        chunk = chunk_;
+        halo = halo_;
+        cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMallocHost(&h_cnt, 4 * sizeof(uint64_t));
+        const uint64_t words = pfac_packed_words(chunk + halo);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            ScanSlot &sl = slot[i];
+            sl.cap = chunk / 8 + 65536;
+            e = cudaMalloc(&sl.text, chunk + halo + 16);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.packed, words * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.out, chunk * 4 + 16);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.cnt, 16);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.ws, compact_workspace_bytes(chunk));
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
+            sl.bad = sl.cnt + 1;
+        }
+        return e;
+    }
+};
+void free_scan_ctx(ScanCtx *c) { delete c; }
+constexpr uint64_t kScanChunk = 1ull << 26;  // 64 Mbases per pipeline chunk
+}  // namespace pfac
+
+extern "C" {
+
+int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, uint64_t n_own, uint64_t n_avail,
+                   uint64_t pos_base, uint64_t *h_pos, uint32_t *h_pid, uint64_t capacity, uint64_t *count,
+                   uint64_t *first_bad) {
+    if (!a || !count) return fail(PFAC_E_ARG, "pfac_scan_host: null automaton / count");
+    if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_scan_host: n_avail < n_own");
+    const uint64_t n = n_own, N = n_avail;  // positions to match; bases readable
+    if (n > 0 && !h_text) return fail(PFAC_E_ARG, "pfac_scan_host: null text");
+    if (capacity > 0 && (!h_pos || !h_pid)) return fail(PFAC_E_ARG, "pfac_scan_host: null h_pos / h_pid");
+    *count = 0;
+    if (n == 0) return PFAC_OK;
+    if (cudaSetDevice(device) != cudaSuccess) return fail(PFAC_E_ARG, "pfac_scan_host: bad device");
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, device, &im);
+    if (rc) return rc;
+    const uint64_t halo = a->maxlen > 0 ? a->maxlen - 1 : 0;
+    {
+        std::lock_guard<std::mutex> lock(const_cast<pfac_automaton *>(a)->mu);
+        if (!im->scan) {
+            auto *ctx = new (std::nothrow) ScanCtx();
+            if (!ctx) return fail(PFAC_E_OOM, "pfac_scan_host: host allocation failed");
+            cudaError_t e = ctx->init(kScanChunk, halo);
+            if (e != cudaSuccess) {
+                delete ctx;
+                return cuda_fail(e, "pfac_scan_host: pipeline allocation");
+            }
+            im->scan = ctx;
+        }
+    }
+    ScanCtx &X = *im->scan;
+    std::lock_guard<std::mutex> lock(X.mu);
+    const uint64_t chunk = X.chunk;
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    cudaStream_t cs = X.cs, xs = X.xs;
+    ScanSlot *slot = X.slot;
+    uint64_t *h_cnt = X.h_cnt;
+    cudaError_t e = cudaSuccess;
+    uint64_t total = 0, bad_at = ~0ull;
+    // enqueue chunk c (copy in, pack, fused match + compact, count + first-bad back to pinned memory)
+    auto enqueue = [&](uint64_t c) -> cudaError_t {
+        ScanSlot &sl = slot[c & 1];
+        const uint64_t s0 = c * chunk, own = (n - s0) < chunk ? (n - s0) : chunk;
+        const uint64_t avail = (N - s0) < own + halo ? (N - s0) : own + halo;
+        cudaError_t r = cudaStreamWaitEvent(xs, sl.done, 0);  // the slot's previous chunk is finished
+        if (r == cudaSuccess) r = cudaMemcpyAsync(sl.text, h_text + s0, avail, cudaMemcpyHostToDevice, xs);
+        if (r == cudaSuccess) r = cudaEventRecord(sl.h2d, xs);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, sl.h2d, 0);
+        if (r == cudaSuccess) r = (cudaError_t)launch_pack(sl.text, avail, sl.packed, pfac_packed_words(avail), sl.bad, cs);
+        if (r == cudaSuccess)
+            r = (cudaError_t)launch_match_compact(*im, a->k, sl.packed, own, avail, sl.out, pos_base + s0, sl.pos,
+                                                  sl.pid, sl.cap, sl.cnt, nullptr, sl.ws, cs);
+        if (r == cudaSuccess) r = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 16, cudaMemcpyDeviceToHost, cs);
+        if (r == cudaSuccess) r = cudaEventRecord(sl.done, cs);
+        return r;
+    };
+    e = enqueue(0);
+    for (uint64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+        if (c + 1 < nchunks) e = enqueue(c + 1);  // next chunk's copy overlaps this chunk's kernels
+        if (e != cudaSuccess) break;
+        ScanSlot &sl = slot[c & 1];
+        e = cudaEventSynchronize(sl.done);
+        if (e != cudaSuccess) break;
+        const uint64_t m = h_cnt[2 * (c & 1)], b = h_cnt[2 * (c & 1) + 1];
+        if (b != ~0ull && bad_at == ~0ull) bad_at = c * chunk + b;
+        if (m > sl.cap) {  // dense chunk: grow this slot's list (kept for later calls) and redo the chunk
+            e = cudaStreamSynchronize(cs);
+            cudaFree(sl.pos);
+            cudaFree(sl.pid);
+            sl.cap = m + 1024;
+            if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
+            if (e == cudaSuccess) e = (cudaError_t)launch_match_compact(
+                *im, a->k, sl.packed, c * chunk + chunk <= n ? chunk : n - c * chunk,
+                (N - c * chunk) < chunk + halo ? N - c * chunk : chunk + halo, sl.out, pos_base + c * chunk, sl.pos,
+                sl.pid, sl.cap, sl.cnt, nullptr, sl.ws, cs);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+            if (e != cudaSuccess) break;
+        }
+        const uint64_t take = total >= capacity ? 0 : (capacity - total < m ? capacity - total : m);
+        if (take) {
+            e = cudaMemcpyAsync(h_pos + total, sl.pos, take * 8, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(h_pid + total, sl.pid, take * 4, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaEventRecord(sl.done, cs);  // the slot is free after these copies
+        }
+        total += m;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(xs);
+    if (e != cudaSuccess) return cuda_fail(e, "pfac_scan_host");
+    *count = total;
+    if (bad_at != ~0ull) {
+        if (first_bad) *first_bad = bad_at;
+        char msg[128];
+        snprintf(msg, sizeof msg, "pfac_scan_host: text byte %llu is not one of ACGTacgt", (unsigned long long)bad_at);
+        return fail(PFAC_E_NON_ACGT, msg);
+    }
+    if (total > capacity) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "pfac_scan_host: %llu matches > capacity %llu", (unsigned long long)total,
                  (unsigned long long)capacity);
         return fail(PFAC_E_CAPACITY, msg);
     }

@@ -65,6 +65,9 @@ struct MatchPlan {
     int sms = 0;
 };
 
+struct ScanCtx;  // pfac_scan_host pipeline resources (api.cu)
+void free_scan_ctx(ScanCtx *c);
+
 // A device image resident on one GPU.
 struct DeviceImage {
     int device = -1;
@@ -78,6 +81,7 @@ struct DeviceImage {
     uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
     uint32_t *d_FB = nullptr;                             // K2 > 0: K1-mer filter bitmap
     size_t l2_persist_bytes = 0;                          // access-policy window over d_J2 (0 = none)
+    ScanCtx *scan = nullptr;                              // created by the first pfac_scan_host
 };
 
 }  // namespace pfac

@@ -2,12 +2,13 @@
 tag=$1; shift
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
   --log-file gpurun_out/launches_${tag}.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/launches_${tag}.log 2>&1
-cap() {  # cap <kernel regex> <out name> <bench args...>
-  local k=$1 name=$2; shift 2
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 \
+cap() {  # cap <kernel regex> <out name> <skip> <bench args...>
+  local k=$1 name=$2 skip=$3; shift 3
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
     -o gpurun_out/${name}_${tag} -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/ncu_${name}_${tag}.log 2>&1
 }
-cap pack_kernel pack_kernel "$@"
-cap match_kernel match_fused "$@"
-cap match_kernel match_kernel --path separate "$@"
-cap compact_kernel compact_kernel --path separate "$@"
+# skip counts: the bench's probe pass launches pack + fused match once before the 3 warm-ups
+cap pack_kernel pack_kernel 4 "$@"
+cap match_kernel match_fused 4 "$@"
+cap match_kernel match_kernel 4 --path separate "$@"
+cap compact_kernel compact_kernel 3 --path separate "$@"

@@ -376,3 +376,39 @@ def test_large_automaton_second_level_jump(lo, hi, k):
     epos, epid = o.match_list(text)
     assert (out == o.match(text)).all() and m == len(epos)
     assert (pos == epos.astype(np.int64)).all() and (pid == epid).all()
+
+
+# --------------------------------------------------------------------------- end to end over host memory
+@pytest.mark.parametrize("n", [1, 1000, (1 << 26) + 12345, (1 << 27) + 3])
+def test_scan_host_chunked(n):
+    """pfac_scan_host streams the host text in 64 Mbase chunks with a halo; list == oracle's."""
+    pats = gen.random_patterns(60, 300, 12, 40)
+    text = gen.plant(gen.iid_text(60, 0, n), 0, n, pats, 60)
+    # a pattern straddling the chunk boundary
+    if n > (1 << 26):
+        text[(1 << 26) - 10:(1 << 26) - 10 + len(pats[0])] = np.frombuffer(pats[0], np.uint8)
+    pos, pid, m = P.scan_host(P.Automaton(pats), torch.from_numpy(text))
+    epos, epid = _oracle_list_parallel(pats, text)
+    assert m == len(epos)
+    assert (pos.numpy() == epos.astype(np.int64)).all() and (pid.numpy() == epid).all()
+
+
+def test_scan_host_dense_and_bad_byte():
+    pats = gen.all_kmers(2)
+    text = gen.iid_text(61, 0, 300_000)
+    pos, pid, m = P.scan_host(P.Automaton(pats), torch.from_numpy(text), pos=torch.empty(10, dtype=torch.int64),
+                              pid=torch.empty(10, dtype=torch.int32))
+    assert m == 300_000 - 1 and (pos.numpy() == np.arange(m)).all()
+    text[123_456] = ord("N")
+    with pytest.raises(B.PfacError) as e:
+        P.scan_host(P.Automaton(pats), torch.from_numpy(text))
+    assert e.value.code == B.E_NON_ACGT
+
+
+def test_scan_host_shard_window():
+    pats = gen.random_patterns(62, 200, 10, 30)
+    n = 400_000
+    text = gen.plant(gen.iid_text(62, 0, n), 0, n, pats, 62)
+    pos, pid, m = P.scan_host(P.Automaton(pats), torch.from_numpy(text), n_own=250_001, pos_base=7)
+    epos, epid = Oracle(pats).match_list(text, 0, 250_001, n=n)
+    assert m == len(epos) and (pos.numpy() == epos.astype(np.int64) + 7).all() and (pid.numpy() == epid).all()
