@@ -26,7 +26,7 @@
 namespace pfac {
 
 #ifndef PFAC_MT
-#define PFAC_MT 640
+#define PFAC_MT 768
 #endif
 #ifndef PFAC_PH1_UNROLL
 #define PFAC_PH1_UNROLL 1
@@ -36,8 +36,14 @@ constexpr int kPh1Unroll = PFAC_PH1_UNROLL; // sub-slices unrolled in the lookup
 constexpr int kMWarps = kMT / 32;
 constexpr uint32_t kP = 8;                  // consecutive positions per lane per sub-slice
 constexpr uint32_t kSubN = 32 * kP;         // 256 positions per sub-slice
-constexpr uint32_t kSlice = 1024;           // positions per warp slice
+#ifndef PFAC_SLICE
+#define PFAC_SLICE 2048
+#endif
+constexpr uint32_t kSlice = PFAC_SLICE;     // positions per warp slice (A/B knob; multiple of 1024)
 constexpr uint32_t kSub = kSlice / kSubN;   // sub-slices per slice
+constexpr uint32_t kHalves = kSlice / 1024; // 1024-position groups (one 32-bit alive mask each)
+constexpr uint32_t kBmWords = kSlice / 32;  // words of the fused kernel's per-slice match bitmap
+static_assert(kSlice % 1024 == 0 && kSlice <= 65536, "slice = whole 1024-position groups, u16 positions");
 
 struct MatchArgs {
     const uint32_t *packed;
@@ -147,7 +153,7 @@ constexpr int kFBK = 10;                            // filter length K1 of uint3
 constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^10 bits = 128 KiB of shared memory  // queue of alive positions (drained to < 32 before it could overflow)
 
 static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
-    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + 128;  // + 1024-bit slice match bitmap
+    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4;  // + slice match bitmap
 }
 
 template <typename CT, bool WIN, int K, bool FUSE, bool FBM>
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         const uint32_t buf = it & 1;
         if (lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
             if (FUSE) {
-            bm[lane] = 0;
+            for (uint32_t w = lane; w < kBmWords; w += 32) bm[w] = 0;
             __syncwarp();
         }
         mbar_wait(&bar[buf], (it >> 1) & 1);
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         };
         // Queue this lane's alive positions (bit r*8+j of `am` = position r*256 + lane*8 + j), one per
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
-        auto push = [&](uint32_t am) {
+        auto push = [&](uint32_t am, uint32_t gbase) {
             while (true) {
                 const uint32_t b = __ballot_sync(~0u, am != 0);
                 if (!b) break;
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 if (am) {
                     const uint32_t bit = __ffs(am) - 1;
                     am &= am - 1;
-                    queue[qn + __popc(b & lt)] = (uint16_t)((bit >> 3) * kSubN + lane * kP + (bit & 7));
+                    queue[qn + __popc(b & lt)] = (uint16_t)(gbase + (bit >> 3) * kSubN + lane * kP + (bit & 7));
                 }
                 qn += __popc(b);
             }
@@ -277,10 +283,12 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         };
         if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K)) {
             // interior slice: every position owned, every K-mer (K1-mer, K2-mer) readable
+#pragma unroll 1
+          for (uint32_t hg = 0; hg < kHalves; ++hg) {
             uint32_t am = 0;
 #pragma unroll kPh1Unroll
-            for (uint32_t r = 0; r < kSub; ++r) {
-                const uint32_t l0 = r * kSubN + lane * kP;
+            for (uint32_t r = 0; r < 4; ++r) {
+                const uint32_t l0 = hg * 1024 + r * kSubN + lane * kP;
                 if constexpr (FBM) {
                     // One filter bit per position: is the K1-mer at l0+j the start of a walk that survives
                     // K1 bases or completes a pattern?  Almost every answer is 0 and stored right away;
@@ -315,22 +323,28 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     }
                 }
             }
-            push(am);
+            push(am, hg * 1024);
+          }
         } else if (FBM) {  // slice at the end of the text: every owned position goes through drain()
+#pragma unroll 1
+          for (uint32_t hg = 0; hg < kHalves; ++hg) {
             uint32_t am = 0;
 #pragma unroll 1
-            for (uint32_t r = 0; r < kSub; ++r) {
-                const uint32_t l0 = r * kSubN + lane * kP;
+            for (uint32_t r = 0; r < 4; ++r) {
+                const uint32_t l0 = hg * 1024 + r * kSubN + lane * kP;
                 if (l0 >= lown) continue;
                 const uint32_t own = lown - l0 >= kP ? 0xFFu : (1u << (lown - l0)) - 1;
                 am |= own << (r * kP);
             }
-            push(am);
+            push(am, hg * 1024);
+          }
         } else {
+#pragma unroll 1
+          for (uint32_t hg = 0; hg < kHalves; ++hg) {
             uint32_t am = 0;
 #pragma unroll 1
-            for (uint32_t r = 0; r < kSub; ++r) {
-                const uint32_t l0 = r * kSubN + lane * kP;
+            for (uint32_t r = 0; r < 4; ++r) {
+                const uint32_t l0 = hg * 1024 + r * kSubN + lane * kP;
                 if (l0 >= lown) continue;
                 uint32_t e[kP];
                 uint32_t alive = 0;
@@ -364,30 +378,34 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 }
                 am |= alive << (r * kP);
             }
-            push(am);
+            push(am, hg * 1024);
+          }
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
-        if (FUSE) {  // stage this slice's matches in position order (lane l owns positions 32l..32l+31)
-            uint32_t w = bm[lane];
-            const uint32_t c = __popc(w);
-            uint32_t incl = c;
+        if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
+#pragma unroll 1
+            for (uint32_t w0 = 0; w0 < kBmWords; w0 += 32) {
+                uint32_t w = bm[w0 + lane];
+                const uint32_t c = __popc(w);
+                uint32_t incl = c;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(~0u, incl, d);
-                if (lane >= (uint32_t)d) incl += y;
-            }
-            uint64_t r = wcount + incl - c;
-            while (w) {
-                const uint32_t bit = __ffs(w) - 1;
-                w &= w - 1;
-                const uint32_t l = lane * 32 + bit;
-                if (r < p.c.stg) {
-                    spos[r] = p.c.pos_base + base + l;
-                    spid[r] = ld_cg_u32(out + l);  // written by this warp before the __syncwarp above
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(~0u, incl, d);
+                    if (lane >= (uint32_t)d) incl += y;
                 }
-                ++r;
+                uint64_t r = wcount + incl - c;
+                while (w) {
+                    const uint32_t bit = __ffs(w) - 1;
+                    w &= w - 1;
+                    const uint32_t l = (w0 + lane) * 32 + bit;
+                    if (r < p.c.stg) {
+                        spos[r] = p.c.pos_base + base + l;
+                        spid[r] = ld_cg_u32(out + l);  // written by this warp before the __syncwarp above
+                    }
+                    ++r;
+                }
+                wcount += __shfl_sync(~0u, incl, 31);
             }
-            wcount += __shfl_sync(~0u, incl, 31);
         }
     }
     if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
