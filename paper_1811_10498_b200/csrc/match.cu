@@ -26,7 +26,7 @@
 namespace pfac {
 
 #ifndef PFAC_MT
-#define PFAC_MT 768
+#define PFAC_MT 896
 #endif
 #ifndef PFAC_PH1_UNROLL
 #define PFAC_PH1_UNROLL 1
