@@ -40,7 +40,6 @@ constexpr uint32_t kSubN = 32 * kP;         // 256 positions per sub-slice
 #define PFAC_SLICE 2048
 #endif
 constexpr uint32_t kSlice = PFAC_SLICE;     // positions per warp slice (A/B knob; multiple of 1024)
-constexpr uint32_t kSub = kSlice / kSubN;   // sub-slices per slice
 constexpr uint32_t kHalves = kSlice / 1024; // 1024-position groups (one 32-bit alive mask each)
 constexpr uint32_t kBmWords = kSlice / 32;  // words of the fused kernel's per-slice match bitmap
 static_assert(kSlice % 1024 == 0 && kSlice <= 65536, "slice = whole 1024-position groups, u16 positions");
@@ -148,7 +147,11 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
     return tb.final_of(s);
 }
 
-constexpr uint32_t kQCap = 128;
+#ifndef PFAC_DRAIN_IPL
+#define PFAC_DRAIN_IPL 1
+#endif
+constexpr uint32_t kDrainIPL = PFAC_DRAIN_IPL;  // queued items per lane per drain round (A/B knob)
+constexpr uint32_t kQCap = 32 * kDrainIPL + 64;  // queue of flagged positions
 constexpr int kFBK = 10;                            // filter length K1 of uint32 images (FBM)
 constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^10 bits = 128 KiB of shared memory  // queue of alive positions (drained to < 32 before it could overflow)
 
@@ -243,25 +246,41 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         auto drain = [&](uint32_t keep) {
             while (qn > keep) {
                 __syncwarp();
-                const uint32_t take = qn - keep < 32 ? qn - keep : 32;
-                if (lane < take) {
-                    const uint32_t l = queue[qn - take + lane];
-                    const uint32_t x = window16(txt, l);
-                    uint32_t res;
-                    if constexpr (FBM) {  // J2 answers the first K2 bases; the rare survivors walk on
-                        if (l + p.K2 <= lend) {
-                            const uint32_t g = __ldg(p.J2 + (x & p.mask2));
-                            res = (g & 0x80000000u) ? walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, lend) : g;
-                        } else {
-                            res = walk(tb, txt, p.root, l, lend);
-                        }
-                    } else {
-                        res = walk(tb, txt, (uint32_t)sJ[x & MASK] & ~ALIVE, l + K, lend);
+                if constexpr (FBM) {
+                    // up to kDrainIPL items per lane per round: all their J2 loads are issued before any is
+                    // consumed, so one L2 round trip serves up to 32 * kDrainIPL positions
+                    const uint32_t avail = qn - keep;
+                    const uint32_t take = avail < 32 * kDrainIPL ? avail : 32 * kDrainIPL;
+                    const uint32_t qb = qn - take;
+                    uint32_t l[kDrainIPL], g[kDrainIPL];
+#pragma unroll
+                    for (uint32_t k = 0; k < kDrainIPL; ++k) {
+                        const uint32_t i = lane + 32 * k;
+                        l[k] = i < take ? queue[qb + i] : 0xFFFFu;
+                        g[k] = (i < take && l[k] + p.K2 <= lend) ? __ldg(p.J2 + (window16(txt, l[k]) & p.mask2))
+                                                                  : 0xFFFFFFFFu;
                     }
-                    out[l] = (int32_t)res;
-                    if (FUSE && res) atomicOr(&bm[l >> 5], 1u << (l & 31));
+#pragma unroll
+                    for (uint32_t k = 0; k < kDrainIPL; ++k) {
+                        if (l[k] == 0xFFFFu) continue;
+                        uint32_t res;
+                        if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], lend);  // last bases of the text
+                        else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, lend);
+                        else res = g[k];
+                        out[l[k]] = (int32_t)res;
+                        if (FUSE && res) atomicOr(&bm[l[k] >> 5], 1u << (l[k] & 31));
+                    }
+                    qn -= take;
+                } else {
+                    const uint32_t take = qn - keep < 32 ? qn - keep : 32;
+                    if (lane < take) {
+                        const uint32_t l = queue[qn - take + lane];
+                        const uint32_t res = walk(tb, txt, (uint32_t)sJ[window16(txt, l) & MASK] & ~ALIVE, l + K, lend);
+                        out[l] = (int32_t)res;
+                        if (FUSE && res) atomicOr(&bm[l >> 5], 1u << (l & 31));
+                    }
+                    qn -= take;
                 }
-                qn -= take;
                 __syncwarp();
             }
         };
@@ -271,7 +290,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             while (true) {
                 const uint32_t b = __ballot_sync(~0u, am != 0);
                 if (!b) break;
-                if (qn + 32 > kQCap) drain(qn & 31);
+                if (qn + 32 > kQCap) drain(qn & 31);  // keep < 32: every drained round is full
                 if (am) {
                     const uint32_t bit = __ffs(am) - 1;
                     am &= am - 1;
