@@ -57,28 +57,38 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     im->maxlen = a->maxlen;
     im->short_pat = h.short_pat;
     im->plan = plan_match(device, h, a->maxlen);
+    // One allocation [J2 | T | F | J | FB] (256-byte aligned parts); the L2 access-policy window
+    // covers the J2 prefix.
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t bJ2 = al(h.J2.size() * 4), bT = al(h.T.size()), bF = al(h.F.size()), bJ = al(h.J.size()),
+                 bFB = al(h.FB.size() * 4);
     cudaError_t e = cudaSetDevice(device);
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_J, h.J.size());
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_T, h.T.size());
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_F, h.F.size());
-    if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_base, bJ2 + bT + bF + bJ + bFB);
+    if (e == cudaSuccess) {
+        uint8_t *b = reinterpret_cast<uint8_t *>(im->d_base);
+        im->d_J2 = h.K2 ? reinterpret_cast<uint32_t *>(b) : nullptr;
+        im->d_T = b + bJ2;
+        im->d_F = b + bJ2 + bT;
+        im->d_J = b + bJ2 + bT + bF;
+        im->d_FB = h.K2 ? reinterpret_cast<uint32_t *>(b + bJ2 + bT + bF + bJ) : nullptr;
+        e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && h.K2) e = cudaMemcpy(im->d_J2, h.J2.data(), h.J2.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && h.K2) e = cudaMemcpy(im->d_FB, h.FB.data(), h.FB.size() * 4, cudaMemcpyHostToDevice);
+    }
     im->K2 = h.K2;
     if (e == cudaSuccess && h.K2) {
-        e = cudaMalloc(&im->d_J2, h.J2.size() * 4);
-        if (e == cudaSuccess) e = cudaMemcpy(im->d_J2, h.J2.data(), h.J2.size() * 4, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMalloc(&im->d_FB, h.FB.size() * 4);
-        if (e == cudaSuccess) e = cudaMemcpy(im->d_FB, h.FB.data(), h.FB.size() * 4, cudaMemcpyHostToDevice);
-        // reserve a persisting L2 set-aside for J2 (device-wide limit; only grown, never shrunk)
+        // persisting L2 set-aside (device-wide limit; only grown, never shrunk) for J2 only: a larger
+        // set-aside (J2 + the T prefix, up to 79 MB) halved cfg4 and slowed the streaming kernels
         int max_persist = 0, max_window = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
-        size_t want = h.J2.size() * 4;
+        size_t want = bJ2;
         if (want > (size_t)max_window) want = (size_t)max_window;
         if (want > (size_t)max_persist) want = (size_t)max_persist;
         size_t cur = 0;
-        if (e == cudaSuccess && want > 0 && cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {
+        if (want > 0 && cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {
             if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
                 cudaGetLastError();
                 want = cur;
@@ -87,11 +97,7 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
         }
     }
     if (e != cudaSuccess) {
-        cudaFree(im->d_J2);
-        cudaFree(im->d_FB);
-        cudaFree(im->d_J);
-        cudaFree(im->d_T);
-        cudaFree(im->d_F);
+        cudaFree(im->d_base);
         delete im;
         return cuda_fail(e, "device image upload");
     }
@@ -119,12 +125,8 @@ void pfac_free(pfac_automaton *a) {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(im->device);
-        cudaFree(im->d_J);
-        cudaFree(im->d_T);
-        cudaFree(im->d_F);
-        cudaFree(im->d_J2);
-        cudaFree(im->d_FB);
         if (im->scan) free_scan_ctx(im->scan);
+        cudaFree(im->d_base);
         cudaSetDevice(prev);
         delete im;
     }

@@ -538,7 +538,7 @@ static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchAr
     }
     if (img.d_J2 && img.l2_persist_bytes) {
         attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[na].val.accessPolicyWindow.base_ptr = img.d_J2;
+        attr[na].val.accessPolicyWindow.base_ptr = img.d_base;  // J2, then the deep-first T rows
         attr[na].val.accessPolicyWindow.num_bytes = img.l2_persist_bytes;
         attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
         attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;

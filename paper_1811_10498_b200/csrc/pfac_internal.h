@@ -77,10 +77,11 @@ struct DeviceImage {
     uint32_t short_pat = 0;
     int K2 = 0;
     MatchPlan plan;
+    void *d_base = nullptr;                               // one allocation: [J2 | T | F | J | FB]
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
     uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
     uint32_t *d_FB = nullptr;                             // K2 > 0: K1-mer filter bitmap
-    size_t l2_persist_bytes = 0;                          // access-policy window over d_J2 (0 = none)
+    size_t l2_persist_bytes = 0;                          // access-policy window from d_base (0 = none)
     ScanCtx *scan = nullptr;                              // created by the first pfac_scan_host
 };
 
