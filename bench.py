@@ -188,9 +188,15 @@ def run_pfac(args):
     from paper_1811_10498_b200.parallel import gather_matches
 
     world, rank, local = dist_env()
+    ndev = torch.cuda.device_count()
     if world > 1:
+        # --backend gloo + more ranks than GPUs exercises the N>1 control flow on one GPU (tests)
+        local = local % ndev
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     t_gen = time.perf_counter()
@@ -271,10 +277,14 @@ def run_pfac(args):
         dist.barrier()
     t_ms = start.elapsed_time(end)
     kt = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evs])  # pack, match, compact
-    t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    t_ms = float(t_max.item())
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t_ms = max_over_ranks(t_ms)
     ms_per_step = t_ms / args.steps
     value = n_total / (ms_per_step * 1e-3) / 1e9
 
@@ -306,10 +316,8 @@ def run_pfac(args):
         t0 = time.perf_counter()
         for _ in range(e_steps):
             mm = e2e_step()
-        te = torch.tensor([(time.perf_counter() - t0) / e_steps * 1e3], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_total / (float(te.item()) * 1e-3) / 1e9, "unit": "Gbases/s",
+        te = max_over_ranks((time.perf_counter() - t0) / e_steps * 1e3)
+        e2e = {"value": n_total / (te * 1e-3) / 1e9, "unit": "Gbases/s",
                "h2d_bytes_per_step": int(n_avail), "d2h_bytes_per_step": int(12 * mm + 16),
                "steps": e_steps, "api": "pfac_scan_host (host memory in and out; wall clock, max over ranks)"}
 
@@ -366,9 +374,11 @@ def main():
     ap.add_argument("--impl", choices=["pfac", "reference"], default="pfac")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process group for N>1 (gloo only to test the multi-rank flow on one GPU)")
     ap.add_argument("--path", choices=["fused", "separate"], default="fused",
                     help="fused: pack -> match+compact kernel; separate: pack -> match -> compact")
-    ap.add_argument("--n", type=int, default=None, help="override bases per rank (testing)")
+    ap.add_argument("--bases-per-rank", dest="n", type=int, default=None, help="override bases per rank (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -56,6 +56,10 @@ def gather_matches(pos, pid, count: int, group=None, dst: int = 0):
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if dist.get_backend(group) == "gloo" and pos.is_cuda:  # gloo collectives run on host tensors
+        hp, hi, counts = gather_matches(pos[:count].cpu(), pid[:count].cpu(), count, group, dst)
+        return (hp.to(pos.device) if hp is not None else None, hi.to(pos.device) if hi is not None else None,
+                counts)
     dev = pos.device
     c = torch.tensor([count], dtype=torch.int64, device=dev)
     counts_t = torch.zeros(world, dtype=torch.int64, device=dev)
