@@ -78,7 +78,11 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
         if (e == cudaSuccess && h.K2) e = cudaMemcpy(im->d_FB, h.FB.data(), h.FB.size() * 4, cudaMemcpyHostToDevice);
     }
     im->K2 = h.K2;
+#ifndef PFAC_NO_PERSIST
     if (e == cudaSuccess && h.K2) {
+#else
+    if (false) {
+#endif
         // persisting L2 set-aside (device-wide limit; only grown, never shrunk) for J2 only: a larger
         // set-aside (J2 + the T prefix, up to 79 MB) halved cfg4 and slowed the streaming kernels
         int max_persist = 0, max_window = 0;

@@ -181,8 +181,8 @@ void derive_host_image(pfac_automaton *a) {
     if (im.cell == 4 || kFilterSmall) {
         std::vector<uint64_t> per_depth(a->maxlen + 2, 0);
         for (uint32_t u = 0; u < S; ++u) per_depth[depth[u]]++;
-        im.K2 = 11;
-        for (int k2 = kFilterK; k2 <= 11; ++k2) {
+        im.K2 = kK2Max;
+        for (int k2 = kK2Min; k2 <= kK2Max; ++k2) {
             const uint64_t D = (uint32_t)k2 < per_depth.size() ? per_depth[k2] : 0;
             if (D * 100 <= 3 * (1ull << (2 * k2))) {
                 im.K2 = k2;

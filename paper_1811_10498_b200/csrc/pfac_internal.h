@@ -21,6 +21,14 @@ constexpr int kFilterK = 10;  // uint32 images: K1-mer filter bitmap, 4^10 bits 
 #define PFAC_FB16 1
 #endif
 constexpr bool kFilterSmall = PFAC_FB16;  // filter + J2 for uint16 images too (A/B knob)
+#ifndef PFAC_K2MAX
+#define PFAC_K2MAX 11
+#endif
+constexpr int kK2Max = PFAC_K2MAX;  // largest second-level jump length (4^11 cells = 16 MiB)
+#ifndef PFAC_K2MIN
+#define PFAC_K2MIN 10
+#endif
+constexpr int kK2Min = PFAC_K2MIN;  // smallest (>= kFilterK: the filter must not look further than J2)
 constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
 
 // Host-side device image: everything the match kernel reads, already in its cell width.
