@@ -152,8 +152,8 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
 #endif
 constexpr uint32_t kDrainIPL = PFAC_DRAIN_IPL;  // queued items per lane per drain round (A/B knob)
 constexpr uint32_t kQCap = 32 * kDrainIPL + 64;  // queue of flagged positions
-constexpr int kFBK = 10;                            // filter length K1 of uint32 images (FBM)
-constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^10 bits = 128 KiB of shared memory  // queue of alive positions (drained to < 32 before it could overflow)
+constexpr int kFBK = kFilterK;                         // filter length K1 (FBM)
+constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared memory (4^10: 128 KiB)
 
 static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
     return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4;  // + slice match bitmap

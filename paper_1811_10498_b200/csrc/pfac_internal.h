@@ -16,7 +16,10 @@ namespace pfac {
 #endif
 constexpr int kJumpK16 = PFAC_K16;  // K for uint16 images: J has 4^8 cells = 128 KiB
 constexpr int kJumpK32 = 7;   // K for uint32 images: J has 4^7 cells = 64 KiB (edge use only)
-constexpr int kFilterK = 10;  // uint32 images: K1-mer filter bitmap, 4^10 bits = 128 KiB
+#ifndef PFAC_FBK
+#define PFAC_FBK 10
+#endif
+constexpr int kFilterK = PFAC_FBK;  // K1-mer filter bitmap, 4^10 bits = 128 KiB (A/B knob)
 #ifndef PFAC_FB16
 #define PFAC_FB16 1
 #endif
@@ -26,7 +29,7 @@ constexpr bool kFilterSmall = PFAC_FB16;  // filter + J2 for uint16 images too (
 #endif
 constexpr int kK2Max = PFAC_K2MAX;  // largest second-level jump length (4^11 cells = 16 MiB)
 #ifndef PFAC_K2MIN
-#define PFAC_K2MIN 10
+#define PFAC_K2MIN PFAC_FBK
 #endif
 constexpr int kK2Min = PFAC_K2MIN;  // smallest (>= kFilterK: the filter must not look further than J2)
 constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
