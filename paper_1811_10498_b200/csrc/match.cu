@@ -147,6 +147,10 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
     return tb.final_of(s);
 }
 
+#ifndef PFAC_CONTIG
+#define PFAC_CONTIG 1
+#endif
+constexpr bool kContiguousSchedule = PFAC_CONTIG;  // unfused kernel: contiguous slice runs per warp (A/B)
 #ifndef PFAC_DRAIN_IPL
 #define PFAC_DRAIN_IPL 1
 #endif
@@ -188,10 +192,11 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     const uint64_t gw = (uint64_t)blockIdx.x * kMWarps + warp;
     // slice schedule: strided over the grid, or (fused) a contiguous run per warp so that the warp's
     // matches come out in position order
-    const uint64_t s_first = FUSE ? gw * p.slices_per_warp : gw;
-    const uint64_t s_end = FUSE ? (s_first + p.slices_per_warp < p.nslices ? s_first + p.slices_per_warp : p.nslices)
-                                : p.nslices;
-    const uint64_t s_stride = FUSE ? 1 : TW;
+    constexpr bool CONTIG = FUSE || kContiguousSchedule;
+    const uint64_t s_first = CONTIG ? gw * p.slices_per_warp : gw;
+    const uint64_t s_end = CONTIG ? (s_first + p.slices_per_warp < p.nslices ? s_first + p.slices_per_warp : p.nslices)
+                                  : p.nslices;
+    const uint64_t s_stride = CONTIG ? 1 : TW;
     auto issue = [&](uint64_t sl, uint32_t *dst, uint64_t *b) {
         const uint64_t w0 = sl * (kSlice / 16);
         const uint64_t left = p.avail_words - w0;
@@ -560,6 +565,7 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_ow
     fill_args(a, img, d_packed, n_own, n_avail, d_out);
     uint64_t grid = (a.nslices + kMWarps - 1) / kMWarps;
     if (grid > (uint64_t)img.plan.sms) grid = img.plan.sms;
+    a.slices_per_warp = (a.nslices + grid * kMWarps - 1) / (grid * kMWarps);
     return launch(img, kernel_for<false>(img), grid, a, false, (cudaStream_t)stream);
 }
 
