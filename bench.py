@@ -228,27 +228,29 @@ def run_pfac(args):
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     fused = args.path == "fused"
+    graph_error = None
     kernels_per_step = 2 if fused else 3
 
-    def step(ev=None):
+    def step(ev=None, st=None):
+        st = stream if st is None else st
         if ev is not None:
-            ev[0].record(stream)
-        P.pack_async(d_text, packed, bad, stream=stream)
+            ev[0].record(st)
+        P.pack_async(d_text, packed, bad, stream=st)
         if ev is not None:
-            ev[1].record(stream)
+            ev[1].record(st)
         if fused:  # match + compact in one kernel
             P.match_compact_async(a, packed, n_own, n_avail, out, pos, pid, count, ws, pos_base=sh.start,
-                                  stream=stream)
+                                  stream=st)
             if ev is not None:
-                ev[2].record(stream)
-                ev[3].record(stream)
+                ev[2].record(st)
+                ev[3].record(st)
         else:
-            P.match_packed_async(a, packed, n_own, n_avail, out, stream=stream)
+            P.match_packed_async(a, packed, n_own, n_avail, out, stream=st)
             if ev is not None:
-                ev[2].record(stream)
-            P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=stream)
+                ev[2].record(st)
+            P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=st)
             if ev is not None:
-                ev[3].record(stream)
+                ev[3].record(st)
         if world > 1:
             m = int(count.item())
             gather_matches(pos, pid, min(m, cap), dst=0)
@@ -261,22 +263,50 @@ def run_pfac(args):
     m_final = int(count.item())
     assert m_final <= cap
 
+    # per-kernel times: K steps with events between the C-ABI calls (also the timed pass without graphs)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with clocks:
-        start.record(stream)
+
+    def timed(run_steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with clocks:
+            start.record(stream)
+            run_steps()
+            end.record(stream)
+            torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        return start.elapsed_time(end)
+
+    def event_steps():
         for i in range(args.steps):
             step(evs[i])
-        end.record(stream)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    t_ms = start.elapsed_time(end)
+
+    graph = None
+    if args.graph and world == 1:  # the step as one CUDA graph (pack + fused kernel, no launch gaps)
+        try:
+            cap_stream = torch.cuda.Stream(dev)
+            cap_stream.wait_stream(stream)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cap_stream):
+                with torch.cuda.graph(graph, stream=cap_stream):
+                    step(None, cap_stream)
+            stream.wait_stream(cap_stream)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as ex:  # noqa: BLE001 - fall back to plain launches, reported in the JSON
+            graph = None
+            graph_error = repr(ex)[:200]
+    kt_ms = timed(event_steps)
     kt = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evs])  # pack, match, compact
+    if graph is not None:
+        clocks = ClockSampler(local)
+        t_ms = timed(lambda: [graph.replay() for _ in range(args.steps)])
+    else:
+        t_ms = kt_ms
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
@@ -349,6 +379,7 @@ def run_pfac(args):
                          "kernel": "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel",
                          "algorithmic_bytes_per_launch": MATCH_BYTES_PER_BASE * n_own, "peak_source": hbm_src},
             "path": args.path,
+            "cuda_graph": graph is not None, **({"cuda_graph_error": graph_error} if graph_error else {}),
             "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,
                            "compact": None if fused else compact_ms,
                            "pack_frac": PACK_BYTES_PER_BASE * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
@@ -374,6 +405,8 @@ def main():
     ap.add_argument("--impl", choices=["pfac", "reference"], default="pfac")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the step's kernels directly instead of replaying one captured CUDA graph")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="process group for N>1 (gloo only to test the multi-rank flow on one GPU)")
     ap.add_argument("--path", choices=["fused", "separate"], default="fused",
