@@ -407,8 +407,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
         if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
+            uint32_t any = 0;
+            for (uint32_t w = lane; w < kBmWords; w += 32) any |= bm[w];
 #pragma unroll 1
-            for (uint32_t w0 = 0; w0 < kBmWords; w0 += 32) {
+            for (uint32_t w0 = 0; w0 < kBmWords && __any_sync(~0u, any); w0 += 32) {
                 uint32_t w = bm[w0 + lane];
                 const uint32_t c = __popc(w);
                 uint32_t incl = c;
