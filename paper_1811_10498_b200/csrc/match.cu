@@ -1,19 +1,26 @@
 // Match kernel: out[i] = id of the longest pattern starting at i.
-//
-// Layout and schedule:
-//  * One persistent CTA of 1024 threads per SM.  Shared memory holds the jump table J (4^K cells),
-//    the first W rows of the device transition table T and of F (all of them when they fit), and
-//    per warp a double-buffered text slice that the warp's lane 0 fetches with a TMA bulk copy.
-//  * A warp owns "slices" of 1024 positions (strided over the grid) + a halo of >= maxlen bases.
-//    Lane l handles 8 consecutive positions of each 256-position sub-slice: one J lookup per
-//    position answers every walk that dies within K bases; the answers are stored right away with
-//    two coalesced st.global.cs.v4 per lane (1 KiB per warp and sub-slice).
-//  * Positions whose walk is still alive after K bases go into a warp-private queue (one ballot per
-//    round gives each lane its slot) and are walked 32 at a time, one per lane, patching out[] after
-//    a __syncwarp.  Unary runs of the trie are "chain rows" that advance over up to 16 forced bases
-//    with one XOR, so a walk rarely needs more than one or two steps after the jump.
 // The walk itself is PAPER.md:91-93 / :204: follow the goto function from the start state, stop at
 // the first missing transition; the answer is the deepest final state passed (F).
+//
+// Layout and schedule (every constant below was chosen by an A/B measurement, the
+// PFAC_* macros are the knobs):
+//  * One persistent CTA of 896 threads per SM.  Shared memory holds the first-level table -- the
+//    4^10-bit filter FB (default) or the jump table J (4^K cells) -- the first W rows of the device
+//    transition table T and of F (all of them when they fit), and per warp a double-buffered text
+//    slice (2048 bases + a halo of >= maxlen bases) that the warp's lane 0 fetches with a TMA bulk
+//    copy (cp.async.bulk + mbarrier).
+//  * Each warp owns a contiguous run of slices.  Lane l handles 8 consecutive positions of each
+//    256-position sub-slice: one 64-bit text window gives the eight 10-mers, one filter bit each.
+//    Unflagged positions answer 0; the zeros are stored right away with two coalesced 16-byte stores
+//    per lane.  (J variant: one J lookup per position answers every walk that dies within K bases.)
+//  * Flagged positions go into a warp-private queue (one ballot per round gives each lane its slot)
+//    and are resolved 32 at a time, one per lane: one L2 load of J2 (the K2-mer jump table, in an
+//    L2-persisting access-policy window) answers the first K2 = 10-11 bases; the few walks still alive
+//    continue over T rows.  Unary runs of the trie are "chain rows" that advance over up to 16 forced
+//    bases with one XOR.  Results patch out[] after a __syncwarp.
+//  * FUSE (pfac_match_compact_async): nonzero results also set bits in a per-slice match bitmap; at
+//    the end of each slice the warp stages its matches in position order, and a grid-wide count
+//    prefix (cooperative launch) places every warp's list.
 #include <cuda_runtime.h>
 
 #include <cstdint>
