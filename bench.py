@@ -28,6 +28,7 @@ METRIC = "Gbases/s per B200 and whole-box at 1/2/4/8 GPUs; % of HBM roofline"
 MATCH_BYTES_PER_BASE = 4.25   # 0.25 B packed text read + 4 B int32 out[] written
 PACK_BYTES_PER_BASE = 1.25    # 1 B ASCII read + 0.25 B packed written
 COMPACT_BYTES_PER_BASE = 4.0  # 4 B out[] read (+12 B per match written)
+BARRIER_BYTES_PER_BASE = 0.125  # --barriers: 2 B mask per 16 bases, written by pack, read by match
 FALLBACK_HBM_GBS = 6650.0     # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -123,7 +124,19 @@ def workload(args, world, rank):
         text = gen.config_text(cfg, 0, sh.avail_end, patterns=pats, n=n_total)[sh.start:]
     else:
         text = gen.config_text(cfg, sh.start, sh.avail_end, patterns=pats, n=n_total)
+    if args.barriers is not None:  # FASTA-like text: newlines + assembly gaps (reading R5)
+        gen.add_barriers(text, cfg.seed, line=args.barriers, a=sh.start, **BARRIER_GAPS)
     return cfg, pats, sh, n_total, text
+
+
+# assembly gaps for --barriers: in 20% of 1 Mbase blocks a run of up to 100 kbases of N (~1% of bytes)
+BARRIER_GAPS = {"block": 1 << 20, "run_max": 100_000, "run_frac": 0.2}
+
+
+def workload_name(cfg, args) -> str:
+    if args.barriers is None:
+        return cfg.name
+    return f"{cfg.name}; FASTA layout: newline every {args.barriers} bases + N gaps (barriers)"
 
 
 def oracle_sample(pats, text, n_own, target_s):
@@ -170,7 +183,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Gbases/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": cfg.name, "n_bases_per_step": m, "patterns": len(pats)},
+        "config": {"workload": workload_name(cfg, args), "n_bases_per_step": m, "patterns": len(pats)},
         "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "Gbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -214,6 +227,8 @@ def run_pfac(args):
     h_text = torch.from_numpy(text).pin_memory()
     d_text = h_text.to(dev)
     packed = torch.empty(P.packed_words(n_avail), dtype=torch.int32, device=dev)
+    bars = args.barriers is not None  # barrier path: pack writes the barrier mask, BAR match kernel
+    inv = torch.empty(P.inv_words(n_avail), dtype=torch.int16, device=dev) if bars else None
     out = torch.empty(n_own, dtype=torch.int32, device=dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
     bad = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -221,8 +236,14 @@ def run_pfac(args):
     # size the list from a probe pass (the count is exact even when the capacity is exceeded)
     pos = torch.empty(1, dtype=torch.int64, device=dev)
     pid = torch.empty(1, dtype=torch.int32, device=dev)
-    P.pack_async(d_text, packed, bad)
-    P.match_compact_async(a, packed, n_own, n_avail, out, pos[:0], pid[:0], count, ws, pos_base=sh.start)
+    def pack(st=None):
+        if bars:
+            P.pack_barriers_async(d_text, packed, inv, bad, stream=st)
+        else:
+            P.pack_async(d_text, packed, bad, stream=st)
+
+    pack()
+    P.match_compact_async(a, packed, n_own, n_avail, out, pos[:0], pid[:0], count, ws, pos_base=sh.start, inv=inv)
     cap = int(count.item()) + 1024
     pos = torch.empty(cap, dtype=torch.int64, device=dev)
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -235,17 +256,20 @@ def run_pfac(args):
         st = stream if st is None else st
         if ev is not None:
             ev[0].record(st)
-        P.pack_async(d_text, packed, bad, stream=st)
+        pack(st)
         if ev is not None:
             ev[1].record(st)
         if fused:  # match + compact in one kernel
             P.match_compact_async(a, packed, n_own, n_avail, out, pos, pid, count, ws, pos_base=sh.start,
-                                  stream=st)
+                                  stream=st, inv=inv)
             if ev is not None:
                 ev[2].record(st)
                 ev[3].record(st)
         else:
-            P.match_packed_async(a, packed, n_own, n_avail, out, stream=st)
+            if bars:
+                P.match_barriers_async(a, packed, inv, n_own, n_avail, out, stream=st)
+            else:
+                P.match_packed_async(a, packed, n_own, n_avail, out, stream=st)
             if ev is not None:
                 ev[2].record(st)
             P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=st)
@@ -258,8 +282,9 @@ def run_pfac(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    # sanity (not a parity claim; tests/ hold those): no bad byte, count fits, first out[] window
-    assert int(bad.item()) == -1
+    # sanity (not a parity claim; tests/ hold those): bad bytes only with --barriers, count fits,
+    # first out[] window
+    assert (int(bad.item()) == -1) != bars
     m_final = int(count.item())
     assert m_final <= cap
 
@@ -322,8 +347,10 @@ def run_pfac(args):
     pack_ms, match_ms, compact_ms = (float(x) for x in kt.mean(axis=0))
     if fused:
         compact_ms = 0.0  # inside the fused kernel
-    match_gbs = MATCH_BYTES_PER_BASE * n_own / (match_ms * 1e-3) / 1e9
-    traffic = profiled_traffic(args.config, args.path) if args.n is None else None
+    match_bpb = MATCH_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
+    pack_bpb = PACK_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
+    match_gbs = match_bpb * n_own / (match_ms * 1e-3) / 1e9
+    traffic = profiled_traffic(args.config, args.path) if args.n is None and not bars else None
 
     # ---- e2e: the same work through the C-ABI's host-memory entry point (pfac_scan_host): the text
     # from pinned HOST memory, chunked H2D overlapped with the kernels, the list copied back to HOST
@@ -369,20 +396,21 @@ def run_pfac(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (seeded SplitMix64 ACGT text, planted patterns; DESIGN.md §3)",
-            "config": {"workload": cfg.name, "n_bases_total": n_total, "n_bases_per_rank": n_own,
+            "config": {"workload": workload_name(cfg, args), "n_bases_total": n_total, "n_bases_per_rank": n_own,
                        "patterns": len(pats), "states": a.num_states, "max_len": a.max_len,
                        "parallelism": f"text-sharded x{world} (halo maxlen-1)",
                        "l2": "inputs larger than L2 (no flush): ASCII text 1 B/base, out[] 4 B/base",
                        "matches_per_step": m_final, "image": a.image_info(local)},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
-                         "kernel": "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel",
-                         "algorithmic_bytes_per_launch": MATCH_BYTES_PER_BASE * n_own, "peak_source": hbm_src},
+                         "kernel": ("match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel")
+                         + ("<BAR=1>" if bars else ""),
+                         "algorithmic_bytes_per_launch": match_bpb * n_own, "peak_source": hbm_src},
             "path": args.path,
             "cuda_graph": graph is not None, **({"cuda_graph_error": graph_error} if graph_error else {}),
             "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,
                            "compact": None if fused else compact_ms,
-                           "pack_frac": PACK_BYTES_PER_BASE * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
+                           "pack_frac": pack_bpb * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
                            "compact_frac": (COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm
                                             if compact_ms > 0 else None)},
             "match_gbases_per_s_per_gpu": n_own / (match_ms * 1e-3) / 1e9,
@@ -412,6 +440,8 @@ def main():
     ap.add_argument("--path", choices=["fused", "separate"], default="fused",
                     help="fused: pack -> match+compact kernel; separate: pack -> match -> compact")
     ap.add_argument("--bases-per-rank", dest="n", type=int, default=None, help="override bases per rank (testing)")
+    ap.add_argument("--barriers", type=int, default=None, metavar="LINE",
+                    help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -89,6 +89,15 @@ uint64_t pfac_packed_words(uint64_t n);
 int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *d_first_bad,
                     void *stream);
 
+/* Pack + barrier map (reading R5): as pfac_pack_async, and
+ * d_inv[w] bit j (j < 16) is set iff text byte 16*w + j is outside ACGTacgt -- a barrier: no walk
+ * crosses it and no pattern occurrence contains it (PAPER.md:91 with SPEC.md:143's reading).
+ * d_inv holds pfac_inv_words(n) uint16 (a multiple of 8, 16-byte aligned; padding words are 0).
+ * Asynchronous. */
+uint64_t pfac_inv_words(uint64_t n);
+int pfac_pack_barriers_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed,
+                             uint16_t *d_inv, uint64_t *d_first_bad, void *stream);
+
 /* ------------------------------------------------------------------------------------------
  * Match (step 4): for every i in [0, n_own): out[i] = id of the longest pattern starting at i
  * whose bases all lie in [0, n_avail) of the packed text, else 0.  n_avail >= n_own
@@ -99,9 +108,20 @@ int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint6
 int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own,
                             uint64_t n_avail, int32_t *d_out, void *stream);
 
-/* Convenience: pack + validate + match over one ASCII text of n bytes (d_out: n int32).
- * Returns PFAC_E_NON_ACGT (out[] unspecified) if the text holds a byte outside ACGTacgt, and then
- * *first_bad (host, nullable) receives its index.  Synchronous. */
+/* Match with barriers: as pfac_match_packed_async, and walks stop at every byte whose d_inv bit is
+ * set (d_inv as written by pfac_pack_barriers_async for n_avail bases), so out[i] = 0 where text
+ * byte i is a barrier and no reported occurrence contains one.  The barrier kernel is an
+ * instantiation of the filter path; an image without the filter (built with PFAC_FB16=0) returns
+ * PFAC_E_CUDA ("operation not supported").  Asynchronous. */
+int pfac_match_barriers_async(const pfac_automaton *a, const uint32_t *d_packed,
+                              const uint16_t *d_inv, uint64_t n_own, uint64_t n_avail,
+                              int32_t *d_out, void *stream);
+
+/* Convenience: pack + match over one ASCII text of n bytes (d_out: n int32).  Bytes outside
+ * ACGTacgt are barriers (reading R5): the call packs with the barrier map, and only when the text
+ * holds such a byte runs the barrier kernel.  *first_bad (host, nullable) receives the index of the
+ * first such byte or UINT64_MAX.  PFAC_E_NON_ACGT only if the text has a barrier and the image has
+ * no filter (PFAC_FB16=0 builds).  Synchronous. */
 int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out,
                uint64_t *first_bad, void *stream);
 
@@ -134,6 +154,12 @@ int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, 
                              uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                              uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist,
                              void *d_workspace, void *stream);
+/* The same with barriers (d_inv as for pfac_match_barriers_async; null = no barriers). */
+int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d_packed,
+                                      const uint16_t *d_inv, uint64_t n_own, uint64_t n_avail,
+                                      int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
+                                      uint32_t *d_pid, uint64_t capacity, uint64_t *d_count,
+                                      uint64_t *d_hist, void *d_workspace, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * End to end over HOST memory (the call a user with a text in RAM makes): the match list
@@ -142,9 +168,11 @@ int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, 
  * in chunks with a (max_len - 1)-base halo: the host-to-device copy of chunk c+1 runs on one stream
  * while chunk c is packed and matched + compacted (fused kernel) on another, and each chunk's list
  * is copied back into h_pos/h_pid at its offset.  Pinned h_text gives copy/compute overlap;
- * pageable memory works too.  Returns PFAC_E_NON_ACGT (the list is then unspecified) if a byte is
- * outside ACGTacgt (*first_bad, nullable, receives its index), PFAC_E_CAPACITY if count > capacity
- * (the first `capacity` entries are written and *count is the total).  Synchronous.
+ * pageable memory works too.  Bytes outside ACGTacgt are barriers (reading R5): a chunk holding one
+ * is re-run with the barrier kernel.  *first_bad (nullable) receives the index (relative to h_text)
+ * of the first such byte read, or UINT64_MAX.  Returns PFAC_E_CAPACITY if count > capacity (the
+ * first `capacity` entries are written and *count is the total), PFAC_E_NON_ACGT only for a barrier
+ * on an image without the filter.  Synchronous.
  */
 int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, uint64_t n_own,
                    uint64_t n_avail, uint64_t pos_base, uint64_t *h_pos, uint32_t *h_pid,

@@ -2,10 +2,14 @@
 
 Public Python surface = the C-ABI of include/pfac.h with the same names (see binding.py):
 ``Automaton`` (pfac_build), ``pack_async``, ``match_packed_async``, ``match``, ``compact_async``,
-``compact``, ``match_compact_async`` (fused), ``scan_host`` (end to end over host memory); ``parallel`` holds the multi-GPU text sharding + NCCL gather.
+``compact``, ``match_compact_async`` (fused), ``scan_host`` (end to end over host memory), and the
+barrier variants ``pack_barriers_async`` / ``match_barriers_async`` (bytes outside ACGT stop walks,
+DESIGN.md reading R5); ``parallel`` holds the multi-GPU text sharding + NCCL gather.
 """
-from .binding import (Automaton, PfacError, compact, compact_async, compact_workspace_bytes, lib, match,
-                      match_compact_async, match_packed_async, pack_async, packed_words, scan_host)
+from .binding import (Automaton, PfacError, compact, compact_async, compact_workspace_bytes, inv_words, lib, match,
+                      match_barriers_async, match_compact_async, match_packed_async, pack_async,
+                      pack_barriers_async, packed_words, scan_host)
 
-__all__ = ["Automaton", "PfacError", "compact", "compact_async", "compact_workspace_bytes", "lib", "match",
-           "match_compact_async", "match_packed_async", "pack_async", "packed_words", "scan_host"]
+__all__ = ["Automaton", "PfacError", "compact", "compact_async", "compact_workspace_bytes", "inv_words", "lib",
+           "match", "match_barriers_async", "match_compact_async", "match_packed_async", "pack_async",
+           "pack_barriers_async", "packed_words", "scan_host"]

@@ -45,6 +45,16 @@ _SIGS = {
                                                 ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_void_p]),
+    "pfac_inv_words": (ctypes.c_uint64, [ctypes.c_uint64]),
+    "pfac_pack_barriers_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_match_barriers_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_match_compact_barriers_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                         ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                                         ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_image_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "pfac_scan_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
@@ -175,6 +185,34 @@ def pack_async(text, packed=None, first_bad=None, stream=None):
     return packed
 
 
+def inv_words(n: int) -> int:
+    return int(lib().pfac_inv_words(n))
+
+
+def pack_barriers_async(text, packed=None, inv=None, first_bad=None, stream=None):
+    """pfac_pack_barriers_async: packed uint32 words + per-word uint16 barrier masks (non-ACGT bytes)."""
+    import torch
+    n = text.numel()
+    if packed is None:
+        packed = torch.empty(packed_words(n), dtype=torch.int32, device=text.device)
+    if inv is None:
+        inv = torch.empty(inv_words(n), dtype=torch.int16, device=text.device)
+    _check(lib().pfac_pack_barriers_async(_ptr(text), n, _ptr(packed), _ptr(inv), _ptr(first_bad),
+                                          _stream(stream, text.device)))
+    return packed, inv
+
+
+def match_barriers_async(a: Automaton, packed, inv, n_own: int, n_avail: int | None = None, out=None, stream=None):
+    """pfac_match_barriers_async: as match_packed_async, walks stop at barrier bytes."""
+    import torch
+    n_avail = n_own if n_avail is None else n_avail
+    if out is None:
+        out = torch.empty(n_own, dtype=torch.int32, device=packed.device)
+    _check(lib().pfac_match_barriers_async(a.handle, _ptr(packed), _ptr(inv), n_own, n_avail, _ptr(out),
+                                           _stream(stream, packed.device)))
+    return out
+
+
 def match_packed_async(a: Automaton, packed, n_own: int, n_avail: int | None = None, out=None, stream=None):
     """pfac_match_packed_async: out[i] for i < n_own, walks bounded by n_avail."""
     import torch
@@ -187,7 +225,7 @@ def match_packed_async(a: Automaton, packed, n_own: int, n_avail: int | None = N
 
 
 def match(a: Automaton, text, out=None, stream=None):
-    """pfac_match: ASCII CUDA tensor -> int32 out (synchronous; raises PfacError on a non-ACGT byte)."""
+    """pfac_match: ASCII CUDA tensor -> int32 out (synchronous; non-ACGT bytes are barriers)."""
     import torch
     n = text.numel()
     if out is None:
@@ -204,8 +242,14 @@ def compact_async(out, pos, pid, count, workspace, pos_base: int = 0, k: int = 0
 
 
 def match_compact_async(a: Automaton, packed, n_own: int, n_avail: int, out, pos, pid, count, workspace,
-                        pos_base: int = 0, hist=None, stream=None):
-    """pfac_match_compact_async: fused match + ordered match list (count: 1-element int64 CUDA tensor)."""
+                        pos_base: int = 0, hist=None, stream=None, inv=None):
+    """pfac_match_compact_async: fused match + ordered match list (count: 1-element int64 CUDA tensor).
+    inv: barrier masks from pack_barriers_async (pfac_match_compact_barriers_async)."""
+    if inv is not None:
+        _check(lib().pfac_match_compact_barriers_async(a.handle, _ptr(packed), _ptr(inv), n_own, n_avail, _ptr(out),
+                                                       pos_base, _ptr(pos), _ptr(pid), pos.numel(), _ptr(count),
+                                                       _ptr(hist), _ptr(workspace), _stream(stream, out.device)))
+        return
     _check(lib().pfac_match_compact_async(a.handle, _ptr(packed), n_own, n_avail, _ptr(out), pos_base, _ptr(pos),
                                           _ptr(pid), pos.numel(), _ptr(count), _ptr(hist), _ptr(workspace),
                                           _stream(stream, out.device)))

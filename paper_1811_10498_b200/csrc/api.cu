@@ -55,6 +55,7 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     im->S = h.S;
     im->root = h.root;
     im->maxlen = a->maxlen;
+    im->minlen = a->minlen;
     im->short_pat = h.short_pat;
     im->plan = plan_match(device, h, a->maxlen);
     // One allocation [J2 | T | F | J | FB] (256-byte aligned parts); the L2 access-policy window
@@ -160,8 +161,22 @@ int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint6
     if (!d_packed || !d_text) return fail(PFAC_E_ARG, "pfac_pack_async: null buffer");
     if (!aligned16(d_packed)) return fail(PFAC_E_ARG, "pfac_pack_async: d_packed must be 16-byte aligned");
     if (device_of(d_packed) < 0) return fail(PFAC_E_ARG, "pfac_pack_async: d_packed is not device memory");
-    int e = launch_pack(d_text, n, d_packed, pfac_packed_words(n), d_first_bad, stream);
+    int e = launch_pack(d_text, n, d_packed, pfac_packed_words(n), d_first_bad, nullptr, stream);
     return e ? cuda_fail(e, "pfac_pack_async") : PFAC_OK;
+}
+
+uint64_t pfac_inv_words(uint64_t n) { return (pfac_packed_words(n) + 7) & ~7ull; }
+
+int pfac_pack_barriers_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint16_t *d_inv,
+                             uint64_t *d_first_bad, void *stream) {
+    if (!d_inv) return fail(PFAC_E_ARG, "pfac_pack_barriers_async: null d_inv");
+    if (n == 0) return pfac_pack_async(d_text, n, d_packed, d_first_bad, stream);
+    if (!d_packed || !d_text) return fail(PFAC_E_ARG, "pfac_pack_barriers_async: null buffer");
+    if (!aligned16(d_packed) || !aligned16(d_inv))
+        return fail(PFAC_E_ARG, "pfac_pack_barriers_async: d_packed and d_inv must be 16-byte aligned");
+    if (device_of(d_packed) < 0) return fail(PFAC_E_ARG, "pfac_pack_barriers_async: d_packed is not device memory");
+    int e = launch_pack(d_text, n, d_packed, pfac_packed_words(n), d_first_bad, d_inv, stream);
+    return e ? cuda_fail(e, "pfac_pack_barriers_async") : PFAC_OK;
 }
 
 int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
@@ -177,41 +192,56 @@ int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, u
     DeviceImage *im = nullptr;
     int rc = get_image(a, dev, &im);
     if (rc) return rc;
-    int e = launch_match(*im, d_packed, n_own, n_avail, d_out, stream);
+    int e = launch_match(*im, d_packed, nullptr, n_own, n_avail, d_out, stream);
     return e ? cuda_fail(e, "pfac_match_packed_async") : PFAC_OK;
+}
+
+int pfac_match_barriers_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv,
+                              uint64_t n_own, uint64_t n_avail, int32_t *d_out, void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match_barriers_async: null automaton");
+    if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_barriers_async: n_avail < n_own");
+    if (n_own == 0) return PFAC_OK;
+    if (!d_packed || !d_out || !d_inv) return fail(PFAC_E_ARG, "pfac_match_barriers_async: null buffer");
+    if (!aligned16(d_packed) || !aligned16(d_out) || !aligned16(d_inv))
+        return fail(PFAC_E_ARG, "pfac_match_barriers_async: buffers must be 16-byte aligned");
+    const int dev = device_of(d_out);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match_barriers_async: d_out is not device memory");
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, dev, &im);
+    if (rc) return rc;
+    int e = launch_match(*im, d_packed, d_inv, n_own, n_avail, d_out, stream);
+    return e ? cuda_fail(e, "pfac_match_barriers_async") : PFAC_OK;
 }
 
 int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out, uint64_t *first_bad,
                void *stream) {
     if (!a) return fail(PFAC_E_ARG, "pfac_match: null automaton");
+    if (first_bad) *first_bad = ~0ull;
     if (n == 0) return PFAC_OK;
     if (!d_text || !d_out) return fail(PFAC_E_ARG, "pfac_match: null buffer");
     if (!aligned16(d_out)) return fail(PFAC_E_ARG, "pfac_match: d_out must be 16-byte aligned");
     const int dev = device_of(d_out);
     if (dev < 0) return fail(PFAC_E_ARG, "pfac_match: d_out is not device memory");
     cudaStream_t st = (cudaStream_t)stream;
-    const uint64_t words = pfac_packed_words(n);
+    const uint64_t words = pfac_packed_words(n), iw = pfac_inv_words(n);
     void *scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, words * 4 + 16, st);
+    cudaError_t e = cudaMallocAsync(&scratch, words * 4 + iw * 2 + 16, st);
     if (e != cudaSuccess) return cuda_fail(e, "pfac_match: scratch allocation");
     uint32_t *d_packed = reinterpret_cast<uint32_t *>(scratch);
-    uint64_t *d_bad = reinterpret_cast<uint64_t *>(d_packed + words);
-    int rc = PFAC_OK;
-    int ce = launch_pack(d_text, n, d_packed, words, d_bad, stream);
+    uint16_t *d_inv = reinterpret_cast<uint16_t *>(d_packed + words);
+    uint64_t *d_bad = reinterpret_cast<uint64_t *>(d_inv + iw);
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, dev, &im);
+    int ce = rc ? 0 : launch_pack(d_text, n, d_packed, words, d_bad, im->K2 ? d_inv : nullptr, stream);
     uint64_t bad = ~0ull;
-    if (!ce) ce = cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st);
-    if (!ce) ce = cudaStreamSynchronize(st);
-    if (!ce && bad != ~0ull) {
+    if (!rc && !ce) ce = cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st);
+    if (!rc && !ce) ce = cudaStreamSynchronize(st);
+    if (!rc && !ce) {
         if (first_bad) *first_bad = bad;
-        char msg[128];
-        snprintf(msg, sizeof msg, "pfac_match: text byte %llu is not one of ACGTacgt", (unsigned long long)bad);
-        rc = fail(PFAC_E_NON_ACGT, msg);
-    }
-    if (!ce && rc == PFAC_OK) {
-        DeviceImage *im = nullptr;
-        rc = get_image(a, dev, &im);
-        if (rc == PFAC_OK) {
-            ce = launch_match(*im, d_packed, n, n, d_out, stream);
+        if (bad != ~0ull && !im->K2) {  // barrier semantics live on the filter path
+            rc = fail(PFAC_E_NON_ACGT, "pfac_match: non-ACGT text needs the filter image (PFAC_FB16=1)");
+        } else {
+            ce = launch_match(*im, d_packed, bad != ~0ull ? d_inv : nullptr, n, n, d_out, stream);
             if (!ce) ce = cudaStreamSynchronize(st);
         }
     }
@@ -222,9 +252,11 @@ int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32
 
 uint64_t pfac_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
 
-int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
-                             int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
-                             uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv,
+                                      uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base,
+                                      uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity, uint64_t *d_count,
+                                      uint64_t *d_hist, void *d_workspace, void *stream) {
+    if (d_inv && !aligned16(d_inv)) return fail(PFAC_E_ARG, "pfac_match_compact_barriers_async: misaligned d_inv");
     if (!a) return fail(PFAC_E_ARG, "pfac_match_compact_async: null automaton");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_compact_async: n_avail < n_own");
     if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_match_compact_async: null d_count / d_workspace");
@@ -239,10 +271,17 @@ int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, 
         int rc = get_image(a, dev, &im);
         if (rc) return rc;
     }
-    int e = n_own > 0 ? launch_match_compact(*im, a->k, d_packed, n_own, n_avail, d_out, pos_base, d_pos, d_pid,
+    int e = n_own > 0 ? launch_match_compact(*im, a->k, d_packed, d_inv, n_own, n_avail, d_out, pos_base, d_pos, d_pid,
                                              capacity, d_count, d_hist, d_workspace, stream)
                       : cudaMemsetAsync(d_count, 0, 8, (cudaStream_t)stream);
     return e ? cuda_fail(e, "pfac_match_compact_async") : PFAC_OK;
+}
+
+int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
+                             int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                             uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+    return pfac_match_compact_barriers_async(a, d_packed, nullptr, n_own, n_avail, d_out, pos_base, d_pos, d_pid,
+                                             capacity, d_count, d_hist, d_workspace, stream);
 }
 
 int pfac_compact_async(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
@@ -296,11 +335,13 @@ namespace pfac {
 struct ScanSlot {
     uint8_t *text = nullptr;
     uint32_t *packed = nullptr;
+    uint16_t *inv = nullptr;  // per-word invalid-base masks (barrier mode, filter images only)
     int32_t *out = nullptr;
     uint64_t *pos = nullptr, *cnt = nullptr, *bad = nullptr;
     uint32_t *pid = nullptr;
     void *ws = nullptr;
     uint64_t cap = 0;
+    bool bar = false;  // this slot's chunk was matched with the barrier kernel
     cudaEvent_t h2d = nullptr, done = nullptr;
 };
 // pfac_scan_host's pipeline resources, kept with the device image and reused across calls.
@@ -314,6 +355,7 @@ struct ScanCtx {
         for (ScanSlot &sl : slot) {
             cudaFree(sl.text);
             cudaFree(sl.packed);
+            cudaFree(sl.inv);
             cudaFree(sl.out);
             cudaFree(sl.pos);
             cudaFree(sl.pid);
@@ -338,6 +380,7 @@ struct ScanCtx {
             sl.cap = chunk / 8 + 65536;
             e = cudaMalloc(&sl.text, chunk + halo + 16);
             if (e == cudaSuccess) e = cudaMalloc(&sl.packed, words * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.inv, pfac_inv_words(chunk + halo) * 2);
             if (e == cudaSuccess) e = cudaMalloc(&sl.out, chunk * 4 + 16);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
@@ -393,6 +436,9 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     uint64_t *h_cnt = X.h_cnt;
     cudaError_t e = cudaSuccess;
     uint64_t total = 0, bad_at = ~0ull;
+    // Barrier kernel or not is predicted from the last chunk whose result is known (a FASTA text has
+    // barriers in every chunk); a chunk that was predicted barrier-free but holds one is re-run.
+    bool predict_bar = false;
     // enqueue chunk c (copy in, pack, fused match + compact, count + first-bad back to pinned memory)
     auto enqueue = [&](uint64_t c) -> cudaError_t {
         ScanSlot &sl = slot[c & 1];
@@ -402,10 +448,14 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
         if (r == cudaSuccess) r = cudaMemcpyAsync(sl.text, h_text + s0, avail, cudaMemcpyHostToDevice, xs);
         if (r == cudaSuccess) r = cudaEventRecord(sl.h2d, xs);
         if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, sl.h2d, 0);
-        if (r == cudaSuccess) r = (cudaError_t)launch_pack(sl.text, avail, sl.packed, pfac_packed_words(avail), sl.bad, cs);
         if (r == cudaSuccess)
-            r = (cudaError_t)launch_match_compact(*im, a->k, sl.packed, own, avail, sl.out, pos_base + s0, sl.pos,
-                                                  sl.pid, sl.cap, sl.cnt, nullptr, sl.ws, cs);
+            r = (cudaError_t)launch_pack(sl.text, avail, sl.packed, pfac_packed_words(avail), sl.bad,
+                                         im->K2 ? sl.inv : nullptr, cs);
+        sl.bar = predict_bar && im->K2;
+        if (r == cudaSuccess)
+            r = (cudaError_t)launch_match_compact(*im, a->k, sl.packed, sl.bar ? sl.inv : nullptr, own, avail,
+                                                  sl.out, pos_base + s0, sl.pos, sl.pid, sl.cap, sl.cnt, nullptr,
+                                                  sl.ws, cs);
         if (r == cudaSuccess) r = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 16, cudaMemcpyDeviceToHost, cs);
         if (r == cudaSuccess) r = cudaEventRecord(sl.done, cs);
         return r;
@@ -417,22 +467,38 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
         ScanSlot &sl = slot[c & 1];
         e = cudaEventSynchronize(sl.done);
         if (e != cudaSuccess) break;
-        const uint64_t m = h_cnt[2 * (c & 1)], b = h_cnt[2 * (c & 1) + 1];
+        uint64_t m = h_cnt[2 * (c & 1)];
+        const uint64_t b = h_cnt[2 * (c & 1) + 1];
         if (b != ~0ull && bad_at == ~0ull) bad_at = c * chunk + b;
-        if (m > sl.cap) {  // dense chunk: grow this slot's list (kept for later calls) and redo the chunk
-            e = cudaStreamSynchronize(cs);
-            cudaFree(sl.pos);
-            cudaFree(sl.pid);
-            sl.cap = m + 1024;
-            if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
-            if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
-            if (e == cudaSuccess) e = (cudaError_t)launch_match_compact(
-                *im, a->k, sl.packed, c * chunk + chunk <= n ? chunk : n - c * chunk,
-                (N - c * chunk) < chunk + halo ? N - c * chunk : chunk + halo, sl.out, pos_base + c * chunk, sl.pos,
-                sl.pid, sl.cap, sl.cnt, nullptr, sl.ws, cs);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
-            if (e != cudaSuccess) break;
+        predict_bar = b != ~0ull;
+        if (b != ~0ull && !im->K2) {
+            e = cudaErrorNotSupported;  // barrier semantics live on the filter path (PFAC_FB16=1)
+            break;
         }
+        // Chunk with barrier bytes: redo it with the barrier kernel.  Dense chunk: grow this slot's
+        // list (kept for later calls) and redo it.  Both run after the next chunk's enqueue, which
+        // touches only the other slot.
+        const uint64_t own = c * chunk + chunk <= n ? chunk : n - c * chunk;
+        const uint64_t avail = (N - c * chunk) < chunk + halo ? N - c * chunk : chunk + halo;
+        for (bool redo = b != ~0ull && !sl.bar; (redo || m > sl.cap) && e == cudaSuccess;) {
+            e = cudaStreamSynchronize(cs);
+            if (m > sl.cap) {
+                cudaFree(sl.pos);
+                cudaFree(sl.pid);
+                sl.cap = m + 1024;
+                if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
+                if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
+            }
+            if (e == cudaSuccess)
+                e = (cudaError_t)launch_match_compact(*im, a->k, sl.packed, b != ~0ull ? sl.inv : nullptr, own, avail,
+                                                      sl.out, pos_base + c * chunk, sl.pos, sl.pid, sl.cap, sl.cnt,
+                                                      nullptr, sl.ws, cs);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 8, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+            m = h_cnt[2 * (c & 1)];
+            redo = false;
+        }
+        if (e != cudaSuccess) break;
         const uint64_t take = total >= capacity ? 0 : (capacity - total < m ? capacity - total : m);
         if (take) {
             e = cudaMemcpyAsync(h_pos + total, sl.pos, take * 8, cudaMemcpyDeviceToHost, cs);
@@ -443,14 +509,11 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(xs);
+    if (e == cudaErrorNotSupported)
+        return fail(PFAC_E_NON_ACGT, "pfac_scan_host: non-ACGT text needs the filter image (PFAC_FB16=1)");
     if (e != cudaSuccess) return cuda_fail(e, "pfac_scan_host");
     *count = total;
-    if (bad_at != ~0ull) {
-        if (first_bad) *first_bad = bad_at;
-        char msg[128];
-        snprintf(msg, sizeof msg, "pfac_scan_host: text byte %llu is not one of ACGTacgt", (unsigned long long)bad_at);
-        return fail(PFAC_E_NON_ACGT, msg);
-    }
+    if (first_bad) *first_bad = bad_at;
     if (total > capacity) {
         char msg[128];
         snprintf(msg, sizeof msg, "pfac_scan_host: %llu matches > capacity %llu", (unsigned long long)total,

@@ -63,6 +63,8 @@ struct MatchArgs {
     const uint32_t *J2;    // second-level jump table (uint32 images), L2-persisting
     const uint32_t *FB;    // uint32 images: the K1-mer filter bitmap (staged in smem instead of J)
     uint32_t K2, mask2;
+    const uint16_t *inv;   // BAR: bit j of inv[w] = base 16w+j is not ACGT (a barrier), pfac_inv_words
+    uint32_t bar_dead;     // BAR: (1 << min(minlen, K1)) - 1: a barrier this close ends every match
     uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
     CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
 };
@@ -166,12 +168,17 @@ constexpr uint32_t kQCap = 32 * kDrainIPL + 64;  // queue of flagged positions
 constexpr int kFBK = kFilterK;                         // filter length K1 (FBM)
 constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared memory (4^10: 128 KiB)
 
-static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words) {
-    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4;  // + slice match bitmap
+static __host__ __device__ constexpr uint32_t inv_buf_words(uint32_t slice_words) {  // uint16, 16-B multiple
+    return (slice_words + 8 + 7) & ~7u;
+}
+static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, bool bar = false) {
+    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4 +  // text, mbarriers, queue, bitmap
+           (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);                // BAR: the slice's barrier bits
 }
 
-template <typename CT, bool WIN, int K, bool FUSE, bool FBM>
+template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
+    static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     CT *sT = reinterpret_cast<CT *>(smem + (FBM ? kFBBytes : NJ * sizeof(CT)));
     CT *sF = sT + (size_t)p.window * 4;
     uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + p.window);  // 16-byte aligned (W % 8 == 0)
-    const uint32_t WB = warp_bytes(p.slice_words);
+    const uint32_t WB = warp_bytes(p.slice_words, BAR);
     uint64_t *tab_bar = reinterpret_cast<uint64_t *>(wbase + kMWarps * WB);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -192,6 +199,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(txt1 + p.slice_words + 4);
     uint16_t *queue = reinterpret_cast<uint16_t *>(bar + 2);
     uint32_t *bm = reinterpret_cast<uint32_t *>(queue + kQCap);  // fused: nonzero cells of the slice
+    uint16_t *inv0 = reinterpret_cast<uint16_t *>(bm + kBmWords);  // BAR: barrier bits of the slice
+    uint16_t *inv1 = inv0 + inv_buf_words(p.slice_words);
     const uint32_t lt = (1u << lane) - 1;
     __shared__ uint64_t s_wcount[kMWarps], s_woff[kMWarps];
 
@@ -208,8 +217,16 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         const uint64_t w0 = sl * (kSlice / 16);
         const uint64_t left = p.avail_words - w0;
         const uint32_t nw = left < p.slice_words ? (uint32_t)left : p.slice_words;
-        mbar_expect_tx(b, nw * 4);
-        bulk_g2s(dst, p.packed + w0, nw * 4, b);
+        if constexpr (BAR) {  // the barrier bits of the same bases ride on the same mbarrier
+            const uint32_t ni = (nw + 7) & ~7u;  // 16-byte multiple (the inv array is padded to 8 words)
+            uint16_t *idst = dst == txt0 ? inv0 : inv1;
+            mbar_expect_tx(b, nw * 4 + ni * 2);
+            bulk_g2s(dst, p.packed + w0, nw * 4, b);
+            bulk_g2s(idst, p.inv + w0, ni * 2, b);
+        } else {
+            mbar_expect_tx(b, nw * 4);
+            bulk_g2s(dst, p.packed + w0, nw * 4, b);
+        }
     };
     if (tid == 0) mbar_init(tab_bar, 1);
     if (lane == 0) {
@@ -245,12 +262,35 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         }
         mbar_wait(&bar[buf], (it >> 1) & 1);
         const uint32_t *txt = buf ? txt1 : txt0;
+        const uint16_t *inv = buf ? inv1 : inv0;
+        (void)inv;
         const uint64_t base = sl * kSlice;
         const uint64_t avail_left = p.n_avail - base;
         const uint32_t lend = avail_left < p.slice_words * 16ull ? (uint32_t)avail_left : p.slice_words * 16;
         const uint64_t own_left = p.n_own - base;
         const uint32_t lown = own_left < kSlice ? (uint32_t)own_left : kSlice;
         int32_t *out = p.out + base;
+        // BAR: does any readable base of this slice (owned range + halo) fail to be ACGT?
+        bool bar_slice = false;
+        if constexpr (BAR) {
+            uint32_t any = 0;
+            for (uint32_t w = lane; w < (lend + 15) / 16; w += 32) any |= inv[w];
+            bar_slice = __any_sync(~0u, any) != 0;
+        }
+        // BAR: local offset of the first barrier at or after l (a walk from l reads bases < it)
+        auto next_barrier = [&](uint32_t l) -> uint32_t {
+            uint32_t q = l >> 4;
+            uint32_t bits = (uint32_t)inv[q] >> (l & 15);
+            uint32_t at = l;
+            while (!bits) {
+                at = (q + 1) * 16;
+                if (at >= lend) return lend;
+                bits = inv[++q];
+            }
+            const uint32_t b = at + (__ffs(bits) - 1);
+            return b < lend ? b : lend;
+        };
+        (void)next_barrier;
 
         uint32_t qn = 0;  // warp-uniform length of the queue of alive positions
         // Walk the queued positions 32 at a time (one per lane) until at most `keep` remain.  The
@@ -264,20 +304,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint32_t avail = qn - keep;
                     const uint32_t take = avail < 32 * kDrainIPL ? avail : 32 * kDrainIPL;
                     const uint32_t qb = qn - take;
-                    uint32_t l[kDrainIPL], g[kDrainIPL];
+                    uint32_t l[kDrainIPL], g[kDrainIPL], le[kDrainIPL];  // le: walk bound (barrier)
 #pragma unroll
                     for (uint32_t k = 0; k < kDrainIPL; ++k) {
                         const uint32_t i = lane + 32 * k;
                         l[k] = i < take ? queue[qb + i] : 0xFFFFu;
-                        g[k] = (i < take && l[k] + p.K2 <= lend) ? __ldg(p.J2 + (window16(txt, l[k]) & p.mask2))
-                                                                  : 0xFFFFFFFFu;
+                        le[k] = (BAR && bar_slice && i < take) ? next_barrier(l[k]) : lend;
+                        g[k] = (i < take && l[k] + p.K2 <= le[k]) ? __ldg(p.J2 + (window16(txt, l[k]) & p.mask2))
+                                                                   : 0xFFFFFFFFu;
                     }
 #pragma unroll
                     for (uint32_t k = 0; k < kDrainIPL; ++k) {
                         if (l[k] == 0xFFFFu) continue;
                         uint32_t res;
-                        if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], lend);  // last bases of the text
-                        else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, lend);
+                        if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], le[k]);  // near the end / a barrier
+                        else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, le[k]);
                         else res = g[k];
                         out[l[k]] = (int32_t)res;
                         if (FUSE && res) atomicOr(&bm[l[k] >> 5], 1u << (l[k] & 31));
@@ -312,7 +353,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
             drain(0);
         };
-        if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K)) {
+        if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K) && !(BAR && bar_slice)) {
             // interior slice: every position owned, every K-mer (K1-mer, K2-mer) readable
 #pragma unroll 1
           for (uint32_t hg = 0; hg < kHalves; ++hg) {
@@ -353,6 +394,48 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         if (nz) atomicOr(&bm[l0 >> 5], nz << (l0 & 31));
                     }
                 }
+            }
+            push(am, hg * 1024);
+          }
+        } else if (BAR && bar_slice) {
+            // Barrier path: a position whose K1-mer window touches a non-ACGT base cannot use the filter;
+            // it is queued with the filter-flagged ones, and drain() bounds every walk at the next
+            // barrier (reading R5: a non-ACGT byte has no transition).  Zeros are stored first.
+#pragma unroll 1
+          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+            uint32_t am = 0;
+#pragma unroll 1
+            for (uint32_t r = 0; r < 4; ++r) {
+                const uint32_t l0 = hg * 1024 + r * kSubN + lane * kP;
+                if (l0 >= lown) continue;
+                const uint32_t own = lown - l0 >= kP ? 0xFFu : (1u << (lown - l0)) - 1;
+                uint32_t m = own;  // default: every owned position goes through drain()
+                if (l0 + kP - 1 + kFBK <= lend) {
+                    const uint32_t q = l0 >> 4, sh = (l0 & 15) * 2;
+                    const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> sh;
+                    const uint32_t ib = (uint32_t)((((uint64_t)inv[q + 2] << 32) | ((uint32_t)inv[q + 1] << 16) |
+                                                    inv[q]) >> (l0 & 15));  // barrier bits of l0..l0+31
+                    m = 0;
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j) {
+                        // A barrier within min(minlen, K1) bases: no pattern fits before it, out = 0.
+                        // Within K1 bases otherwise: the filter cannot answer, the walk in drain() does.
+                        const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
+                        const uint32_t bj = ib >> j;
+                        const bool near = bj & ((1u << kFBK) - 1);
+                        const bool flag = near ? !(bj & p.bar_dead) : ((sFB[idx >> 5] >> (idx & 31)) & 1u);
+                        m |= flag ? (1u << j) : 0u;
+                    }
+                    m &= own;
+                }
+                if (l0 + kP <= lown) {
+                    st_stream_v4(out + l0, 0u, 0u, 0u, 0u);
+                    st_stream_v4(out + l0 + 4, 0u, 0u, 0u, 0u);
+                } else {
+                    for (uint32_t j = 0; j < kP; ++j)
+                        if (l0 + j < lown) out[l0 + j] = 0;
+                }
+                am |= m << (r * kP);
             }
             push(am, hg * 1024);
           }
@@ -474,8 +557,9 @@ static void dev_props(int device, int &sms, int &optin) {
 
 constexpr size_t kStaticSmemReserve = 1024;  // the fused kernel's static shared arrays (grid_prefix)
 
-static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words) {
-    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words) + 16;
+static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
+                         bool bar = false) {
+    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words, bar) + 16;
 }
 
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
@@ -491,6 +575,13 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     pl.all_smem = w >= h.rows;
     pl.window = pl.all_smem ? h.rows : w;
     pl.smem = match_smem(table, pl.cell, pl.window, pl.slice_words);
+    // barrier-mode variant (BAR): per-warp barrier bits take room from the row window
+    const size_t fixed_b = match_smem(table, pl.cell, 0, pl.slice_words, true) + kStaticSmemReserve;
+    const size_t budget_b = (size_t)optin > fixed_b ? (size_t)optin - fixed_b : 0;
+    const uint32_t wb = (uint32_t)(budget_b / (5 * pl.cell)) & ~7u;
+    pl.all_smem_bar = wb >= h.rows;
+    pl.window_bar = pl.all_smem_bar ? h.rows : wb;
+    pl.smem_bar = match_smem(table, pl.cell, pl.window_bar, pl.slice_words, true);
     pl.sms = sms;
     return pl;
 }
@@ -510,17 +601,25 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.root = img.root;
     a.slice_words = img.plan.slice_words;
     a.short_pat = img.short_pat;
+    a.bar_dead = (1u << (img.minlen < (uint32_t)kFBK ? img.minlen : (uint32_t)kFBK)) - 1;
     a.J2 = img.d_J2;
     a.FB = img.d_FB;
     a.K2 = (uint32_t)img.K2;
     a.mask2 = img.K2 ? (uint32_t)((1ull << (2 * img.K2)) - 1) : 0u;
     a.slices_per_warp = 0;
+    a.inv = nullptr;
     a.c = CompactArgs{};
 }
 
 template <bool FUSE>
-static const void *kernel_for(const DeviceImage &img) {
+static const void *kernel_for(const DeviceImage &img, bool bar) {
     const MatchPlan &pl = img.plan;
+    if (bar) {  // barrier semantics (non-ACGT bytes present): filter path only
+        if (pl.cell == 2) return pl.all_smem_bar ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, true, true>
+                                                 : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE, true, true>;
+        return pl.all_smem_bar ? (const void *)match_kernel<uint32_t, false, kJumpK32, FUSE, true, true>
+                               : (const void *)match_kernel<uint32_t, true, kJumpK32, FUSE, true, true>;
+    }
     if (pl.cell == 2 && img.K2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, true>
                                                    : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE, true>;
     if (pl.cell == 2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, false>
@@ -536,12 +635,14 @@ static const void *kernel_for(const DeviceImage &img) {
 static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchArgs &a, bool cooperative,
                   cudaStream_t st) {
     const MatchPlan &pl = img.plan;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    const size_t smem = a.inv ? pl.smem_bar : pl.smem;
+    if (a.inv) a.window = pl.window_bar;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kMT);
-    cfg.dynamicSmemBytes = pl.smem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -567,25 +668,30 @@ static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchAr
     return cudaGetLastError();
 }
 
-int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
-                 int32_t *d_out, void *stream) {
+int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_t *d_inv, uint64_t n_own,
+                 uint64_t n_avail, int32_t *d_out, void *stream) {
     if (n_own == 0) return cudaSuccess;
     MatchArgs a;
     fill_args(a, img, d_packed, n_own, n_avail, d_out);
+    if (d_inv && !img.K2) return cudaErrorNotSupported;  // barrier mode lives on the filter path
+    a.inv = d_inv;
     uint64_t grid = (a.nslices + kMWarps - 1) / kMWarps;
     if (grid > (uint64_t)img.plan.sms) grid = img.plan.sms;
     a.slices_per_warp = (a.nslices + grid * kMWarps - 1) / (grid * kMWarps);
-    return launch(img, kernel_for<false>(img), grid, a, false, (cudaStream_t)stream);
+    return launch(img, kernel_for<false>(img, d_inv != nullptr), grid, a, false, (cudaStream_t)stream);
 }
 
 // Fused match + compact: out[] and the ordered match list in one pass.
-int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, uint64_t n_own,
-                         uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
-                         uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
+                         uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
+                         uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
+                         void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_own == 0) return cudaMemsetAsync(d_count, 0, 8, st);
     MatchArgs a;
     fill_args(a, img, d_packed, n_own, n_avail, d_out);
+    if (d_inv && !img.K2) return cudaErrorNotSupported;
+    a.inv = d_inv;
     const MatchPlan &pl = img.plan;
     const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
     const uint64_t warps = grid * kMWarps;
@@ -608,7 +714,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.chunk = a.slices_per_warp * kSlice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    return launch(img, kernel_for<true>(img), grid, a, true, st);
+    return launch(img, kernel_for<true>(img, d_inv != nullptr), grid, a, true, st);
 }
 
 }  // namespace pfac

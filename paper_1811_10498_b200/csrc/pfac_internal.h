@@ -73,6 +73,9 @@ struct MatchPlan {
     uint32_t window = 0;       // device ids [0, window) staged in shared memory
     uint32_t slice_words = 0;  // packed words per warp slice (512 bases + halo)
     size_t smem = 0;           // dynamic shared memory per CTA
+    bool all_smem_bar = false; // the same three for the barrier-mode variant (BAR)
+    uint32_t window_bar = 0;
+    size_t smem_bar = 0;
     int sms = 0;
 };
 
@@ -84,7 +87,7 @@ struct DeviceImage {
     int device = -1;
     int K = kJumpK32;
     uint32_t S = 0, root = 0;
-    uint32_t maxlen = 0;
+    uint32_t maxlen = 0, minlen = 0;
     uint32_t short_pat = 0;
     int K2 = 0;
     MatchPlan plan;
@@ -121,15 +124,16 @@ void derive_host_image(pfac_automaton *a);
 
 // kernels.cu launchers (all asynchronous on `stream`); return cudaError_t as int.
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,
-                uint64_t *d_first_bad, void *stream);
-int launch_match(const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
-                 int32_t *d_out, void *stream);
+                uint64_t *d_first_bad, uint16_t *d_inv, void *stream);
+int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_t *d_inv, uint64_t n_own,
+                 uint64_t n_avail, int32_t *d_out, void *stream);
 int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                    uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,
                    void *stream);
 uint64_t compact_workspace_bytes(uint64_t n);
-int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, uint64_t n_own,
-                         uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
-                         uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream);
+int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
+                         uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
+                         uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
+                         void *stream);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 }  // namespace pfac

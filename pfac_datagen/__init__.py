@@ -176,6 +176,41 @@ def plant(text: np.ndarray, a: int, n_total: int, patterns: list[bytes], seed: i
     return text
 
 
+# --------------------------------------------------------------------------- barriers (reading R5)
+BARRIER_BYTES = np.frombuffer(b"NNNNNNRYKMn-", dtype=np.uint8)
+
+
+def add_barriers(text: np.ndarray, seed: int, line: int = 80, block: int = 4096, run_max: int = 300,
+                 run_frac: float = 0.25, a: int = 0) -> np.ndarray:
+    """FASTA-like barriers over ``text`` = bases [a, a+len(text)) in place: a newline after every
+    ``line`` bases (global positions g with g mod (line+1) == line; line = 0: none) and, in a
+    ``run_frac`` share of the ``block``-base blocks, one run of 1..run_max bytes drawn from
+    BARRIER_BYTES (mostly 'N', the assembly-gap code) at a random offset.  Holds none of the method's
+    arithmetic; both the oracle and the CUDA path read the result."""
+    n = len(text)
+    if n == 0:
+        return text
+    b = a + n
+    if line > 0:
+        first = a + (line - a % (line + 1)) % (line + 1)
+        text[first - a::line + 1] = ord("\n")
+    blk0 = max(0, (a - run_max - block) // block)
+    blk1 = (b - 1) // block + 1
+    nb = blk1 - blk0
+    key = substream_key(seed, "barriers")
+    r, r2 = u64(key, blk0, nb), u64(key, (1 << 40) + blk0, nb)
+    pick = (r >> np.uint64(11)).astype(np.float64) / float(1 << 53) < run_frac
+    ln = (r % np.uint64(run_max)).astype(np.int64) + 1
+    off = ((r2 >> np.uint64(32)) % np.uint64(block)).astype(np.int64)
+    code = (r2 % np.uint64(len(BARRIER_BYTES))).astype(np.int64)
+    for j in np.nonzero(pick)[0].tolist():
+        s = (blk0 + j) * block + int(off[j])
+        lo, hi = max(s, a), min(b, s + int(ln[j]))
+        if lo < hi:
+            text[lo - a:hi - a] = BARRIER_BYTES[int(code[j])]
+    return text
+
+
 # --------------------------------------------------------------------------- config 5 (repetitive)
 def _primitive(u: bytes) -> bool:
     n = len(u)

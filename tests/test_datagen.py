@@ -51,3 +51,20 @@ def test_exhausted_length_classes_terminate():
     import pytest
     with pytest.raises(ValueError):
         gen.random_patterns(1, 30, 1, 2)  # only 4 + 16 = 20 distinct patterns exist
+
+
+def bad_at(t):
+    return ~np.isin(t, np.frombuffer(b"ACGT", np.uint8))
+
+
+def test_add_barriers_windows_and_layout():
+    """Barrier placement depends on global positions only (shards see the same bytes as the whole)."""
+    n = 300_000
+    full = gen.add_barriers(gen.iid_text(1, 0, n), 1, line=60, block=2048, run_max=3000, run_frac=0.4)
+    for a, b in [(0, 1000), (12_345, 200_000), (150_000, n), (n - 1, n)]:
+        part = gen.add_barriers(gen.iid_text(1, a, b), 1, line=60, block=2048, run_max=3000, run_frac=0.4, a=a)
+        assert (part == full[a:b]).all()
+    assert bad_at(full)[60::61].all() and (full[60::61] == ord("\n")).mean() > 0.5  # runs may cover a newline
+    bad = bad_at(full)
+    assert set(np.unique(full[bad]).tolist()) <= set(gen.BARRIER_BYTES.tolist()) | {ord("\n")}
+    assert 0.05 < (full == ord("N")).mean() < 0.5
