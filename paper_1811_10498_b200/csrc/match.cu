@@ -415,17 +415,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> sh;
                     const uint32_t ib = (uint32_t)((((uint64_t)inv[q + 2] << 32) | ((uint32_t)inv[q + 1] << 16) |
                                                     inv[q]) >> (l0 & 15));  // barrier bits of l0..l0+31
-                    m = 0;
+                    // near (bit j): a barrier within K1 bases of l0+j -- the filter cannot answer, the
+                    // walk in drain() does; dead: a barrier within min(minlen, K1) bases -- no pattern
+                    // fits before it, out = 0.  Both as smears of the barrier bits, branch-free.
+                    uint32_t fb = 0, near = 0, dead = 0;
 #pragma unroll
                     for (uint32_t j = 0; j < kP; ++j) {
-                        // A barrier within min(minlen, K1) bases: no pattern fits before it, out = 0.
-                        // Within K1 bases otherwise: the filter cannot answer, the walk in drain() does.
                         const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
-                        const uint32_t bj = ib >> j;
-                        const bool near = bj & ((1u << kFBK) - 1);
-                        const bool flag = near ? !(bj & p.bar_dead) : ((sFB[idx >> 5] >> (idx & 31)) & 1u);
-                        m |= flag ? (1u << j) : 0u;
+                        fb |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
                     }
+#pragma unroll
+                    for (uint32_t t = 0; t < (uint32_t)kFBK; ++t) {
+                        near |= ib >> t;
+                        dead |= (ib >> t) & (0u - ((p.bar_dead >> t) & 1u));
+                    }
+                    m = ((fb & ~near) | (near & ~dead)) & 0xFFu;
                     m &= own;
                 }
                 if (l0 + kP <= lown) {
