@@ -12,3 +12,4 @@ cap pack_kernel pack_kernel 4 "$@"
 cap match_kernel match_fused 4 "$@"
 cap match_kernel match_kernel 4 --path separate "$@"
 cap compact_kernel compact_kernel 3 --path separate "$@"
+cap match_kernel match_bar 4 --barriers 80 "$@"
