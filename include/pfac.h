@@ -178,6 +178,32 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
                    uint64_t n_avail, uint64_t pos_base, uint64_t *h_pos, uint32_t *h_pid,
                    uint64_t capacity, uint64_t *count, uint64_t *first_bad);
 
+/* ------------------------------------------------------------------------------------------
+ * All occurrences: the set the serial Aho-Corasick machine reports
+ * (PAPER.md:77, :87), from PFAC's longest-only list.  Every pattern occurring at i is a prefix of
+ * the longest one there, so the set is {(i, q) : (i, p) in the list, q on the prefix chain of p}.
+ * pfac_prefix_chain(a): host array of 2*(k+1) uint32 owned by `a`: [2p] = id of the longest pattern
+ * that is a proper prefix of pattern p (0 = none), [2p+1] = length of p's chain (p included);
+ * entries for p = 0 are 0.
+ * pfac_expand_async: reads m = min(*d_count, in_capacity) entries (d_pos uint64 / d_pid uint32,
+ * e.g. pfac_compact_async's output with its d_count) and writes the occurrences in ascending
+ * position and, at one position, ascending pattern length: the first min(total, capacity) into
+ * d_pos_all / d_pid_all, the total into *d_count_all (device).  pid values 0 or > k contribute
+ * nothing.  d_workspace holds pfac_expand_workspace_bytes() bytes (reset by the call).
+ * Asynchronous (a cooperative launch).
+ * pfac_expand: `count` input entries (host value), *count_all on the host; PFAC_E_CAPACITY if the
+ * total exceeds capacity (the first `capacity` entries are written).  Synchronous.
+ */
+const uint32_t *pfac_prefix_chain(const pfac_automaton *a);
+uint64_t pfac_expand_workspace_bytes(void);
+int pfac_expand_async(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *d_pid,
+                      const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all,
+                      uint32_t *d_pid_all, uint64_t capacity, uint64_t *d_count_all,
+                      void *d_workspace, void *stream);
+int pfac_expand(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *d_pid,
+                uint64_t count, uint64_t *d_pos_all, uint32_t *d_pid_all, uint64_t capacity,
+                uint64_t *count_all, void *stream);
+
 /* Device image facts for reports and tests; builds the image if needed. */
 typedef struct {
     int32_t device;

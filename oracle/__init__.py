@@ -9,6 +9,7 @@ Contents (each function cites the passage it follows):
 * ``Oracle`` — O2, the bit-exactness reference: the paper's insertion-order 4 x N transition
   table (Table 1) walked failure-lessly from every text position
   (PAPER.md:91-93, :204).  Implemented in plain C (``pfac_oracle.c``), loaded with ctypes.
+  ``Oracle.match_all`` emits every pattern the walk completes (all occurrences, ascending length).
 * ``bruteforce.longest_at`` — O1, the plain definition by direct substring comparison.
 * ``classic_ac`` — O3, the serial Aho-Corasick machine with goto/failure/output
   (PAPER.md:62-87), whose all-occurrence set must equal ``expand(out)``.
@@ -63,6 +64,8 @@ def lib():
         L.oracle_match_list.argtypes = [vp, u8p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                         u64p, u32p, ctypes.c_uint64]
         L.oracle_match_list.restype = ctypes.c_uint64
+        L.oracle_match_all.argtypes = L.oracle_match_list.argtypes
+        L.oracle_match_all.restype = ctypes.c_uint64
         _lib = L
     return _lib
 
@@ -152,6 +155,26 @@ class Oracle:
             if b > a:
                 m = int(lib().oracle_match_list(self._h, _ptr(t, ctypes.c_uint8), n, a, b,
                                                 _ptr(pos, ctypes.c_uint64), _ptr(pid, ctypes.c_uint32), cap))
+            if m <= cap:
+                return pos[:m], pid[:m]
+            cap = m
+
+
+    def match_all(self, text, a: int = 0, b: int | None = None, n: int | None = None,
+                  cap: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """Every occurrence (pos uint64, pid uint32) starting in [a, b): ascending position, then
+        ascending pattern length (pfac_oracle.c oracle_match_all)."""
+        t = _as_u8(text)
+        n = len(t) if n is None else n
+        b = n if b is None else b
+        cap = max(1, (b - a) // 32 + 1024) if cap is None else cap
+        while True:
+            pos = np.zeros(cap, dtype=np.uint64)
+            pid = np.zeros(cap, dtype=np.uint32)
+            m = 0
+            if b > a:
+                m = int(lib().oracle_match_all(self._h, _ptr(t, ctypes.c_uint8), n, a, b,
+                                               _ptr(pos, ctypes.c_uint64), _ptr(pid, ctypes.c_uint32), cap))
             if m <= cap:
                 return pos[:m], pid[:m]
             cap = m

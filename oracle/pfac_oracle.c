@@ -161,3 +161,27 @@ uint64_t oracle_match_list(const oracle_trie *t, const uint8_t *text, uint64_t n
     }
     return m;
 }
+
+/* Every occurrence: the walk of position i passes the final state of
+ * every pattern that occurs at i, since each such pattern's bases are the first bases of the walk
+ * (PAPER.md:91-93); emitting each completed id as the walk goes gives the occurrences at i in
+ * ascending length.  For i in [a, b), ascending i; writes at most cap entries, returns the total. */
+uint64_t oracle_match_all(const oracle_trie *t, const uint8_t *text, uint64_t n, uint64_t a,
+                          uint64_t b, uint64_t *pos, uint32_t *pid, uint64_t cap) {
+    uint64_t m = 0;
+    for (uint64_t i = a; i < b; ++i) {
+        uint32_t s = 0;
+        for (uint64_t j = i; j < n; ++j) {
+            int col = column_of(text[j]);
+            if (col < 0) break;
+            cell_t c = t->rows[(size_t)s * 4 + col];
+            if (c.next == 0) break;
+            if (c.pid != 0) {
+                if (m < cap) { pos[m] = i; pid[m] = c.pid; }
+                ++m;
+            }
+            s = c.next;
+        }
+    }
+    return m;
+}

@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libpfac.so")
-SOURCES = ["api.cu", "match.cu", "pack.cu", "compact.cu", "builder.cpp"]
+SOURCES = ["api.cu", "match.cu", "pack.cu", "compact.cu", "expand.cu", "builder.cpp"]
 HEADERS = ["pfac_internal.h", "ptx.cuh", os.path.join("..", "..", "include", "pfac.h")]
 
 NVCC_FLAGS = [

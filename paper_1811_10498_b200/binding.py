@@ -55,6 +55,14 @@ _SIGS = {
                                                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                                          ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_prefix_chain": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "pfac_expand_workspace_bytes": (ctypes.c_uint64, []),
+    "pfac_expand_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_expand": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                   ctypes.c_void_p]),
     "pfac_image_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "pfac_scan_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
@@ -159,6 +167,12 @@ class Automaton:
 
     def prepare(self, device: int = 0) -> None:
         _check(lib().pfac_prepare(self._h, device))
+
+    def prefix_chain(self) -> np.ndarray:
+        """pfac_prefix_chain: (k+1) x 2 uint32 [longest proper-prefix pattern id, chain length]."""
+        k = self.num_patterns
+        p = lib().pfac_prefix_chain(self._h)
+        return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint32)), shape=(k + 1, 2)).copy()
 
     def image_info(self, device: int = 0) -> dict:
         """pfac_image_info: the device image's layout facts (builds the image if needed)."""
@@ -304,3 +318,34 @@ def compact(out, pos_base: int = 0, capacity: int | None = None, k: int = 0, his
         _check(rc)
         m = int(c.value)
         return pos[:m], pid[:m], m
+
+
+def expand_workspace_bytes() -> int:
+    return int(lib().pfac_expand_workspace_bytes())
+
+
+def expand_async(a: Automaton, pos, pid, count, pos_all, pid_all, count_all, workspace, stream=None):
+    """pfac_expand_async: every occurrence from the longest-only list (count/count_all: 1-element int64
+    CUDA tensors; the input is the first min(count, pos.numel()) entries)."""
+    _check(lib().pfac_expand_async(a.handle, _ptr(pos), _ptr(pid), _ptr(count), pos.numel(), _ptr(pos_all),
+                                   _ptr(pid_all), pos_all.numel(), _ptr(count_all), _ptr(workspace),
+                                   _stream(stream, count_all.device)))
+
+
+def expand(a: Automaton, pos, pid, capacity: int | None = None, stream=None):
+    """pfac_expand: (pos_all int64, pid_all int32, total) trimmed to total (synchronous)."""
+    import torch
+    m = pos.numel()
+    cap = max(1024, 2 * m) if capacity is None else capacity
+    while True:
+        pa = torch.empty(max(cap, 1), dtype=torch.int64, device=pos.device)
+        pi = torch.empty(max(cap, 1), dtype=torch.int32, device=pos.device)
+        c = ctypes.c_uint64(0)
+        rc = lib().pfac_expand(a.handle, _ptr(pos), _ptr(pid), m, _ptr(pa), _ptr(pi), cap, ctypes.byref(c),
+                               _stream(stream, pos.device))
+        if rc == E_CAPACITY and capacity is None:
+            cap = int(c.value)
+            continue
+        _check(rc)
+        t = int(c.value)
+        return pa[:t], pi[:t], t

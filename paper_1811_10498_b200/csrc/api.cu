@@ -62,9 +62,9 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     // covers the J2 prefix.
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t bJ2 = al(h.J2.size() * 4), bT = al(h.T.size()), bF = al(h.F.size()), bJ = al(h.J.size()),
-                 bFB = al(h.FB.size() * 4);
+                 bFB = al(h.FB.size() * 4), bC = al(a->chain.size() * 4);
     cudaError_t e = cudaSetDevice(device);
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_base, bJ2 + bT + bF + bJ + bFB);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_base, bJ2 + bT + bF + bJ + bFB + bC);
     if (e == cudaSuccess) {
         uint8_t *b = reinterpret_cast<uint8_t *>(im->d_base);
         im->d_J2 = h.K2 ? reinterpret_cast<uint32_t *>(b) : nullptr;
@@ -72,7 +72,11 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
         im->d_F = b + bJ2 + bT;
         im->d_J = b + bJ2 + bT + bF;
         im->d_FB = h.K2 ? reinterpret_cast<uint32_t *>(b + bJ2 + bT + bF + bJ) : nullptr;
-        e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
+        im->d_chain = reinterpret_cast<const uint32_t *>(b + bJ2 + bT + bF + bJ + bFB);
+        e = cudaMemcpy(const_cast<uint32_t *>(im->d_chain), a->chain.data(), a->chain.size() * 4,
+                       cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess && h.K2) e = cudaMemcpy(im->d_J2, h.J2.data(), h.J2.size() * 4, cudaMemcpyHostToDevice);
@@ -517,6 +521,67 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     if (total > capacity) {
         char msg[128];
         snprintf(msg, sizeof msg, "pfac_scan_host: %llu matches > capacity %llu", (unsigned long long)total,
+                 (unsigned long long)capacity);
+        return fail(PFAC_E_CAPACITY, msg);
+    }
+    return PFAC_OK;
+}
+
+const uint32_t *pfac_prefix_chain(const pfac_automaton *a) { return a ? a->chain.data() : nullptr; }
+
+uint64_t pfac_expand_workspace_bytes(void) { return expand_workspace_bytes(); }
+
+int pfac_expand_async(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *d_pid, const uint64_t *d_count,
+                      uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all, uint64_t capacity,
+                      uint64_t *d_count_all, void *d_workspace, void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_expand_async: null automaton");
+    if (!d_count || !d_count_all || !d_workspace)
+        return fail(PFAC_E_ARG, "pfac_expand_async: null d_count / d_count_all / d_workspace");
+    if (in_capacity > 0 && (!d_pos || !d_pid)) return fail(PFAC_E_ARG, "pfac_expand_async: null d_pos / d_pid");
+    if (capacity > 0 && (!d_pos_all || !d_pid_all))
+        return fail(PFAC_E_ARG, "pfac_expand_async: null d_pos_all / d_pid_all");
+    const int dev = device_of(d_count_all);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_expand_async: d_count_all is not device memory");
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, dev, &im);
+    if (rc) return rc;
+    int e = launch_expand(*im, a->k, d_pos, d_pid, d_count, in_capacity, d_pos_all, d_pid_all, capacity, d_count_all,
+                          d_workspace, stream);
+    return e ? cuda_fail(e, "pfac_expand_async") : PFAC_OK;
+}
+
+int pfac_expand(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *d_pid, uint64_t count,
+                uint64_t *d_pos_all, uint32_t *d_pid_all, uint64_t capacity, uint64_t *count_all, void *stream) {
+    if (!count_all) return fail(PFAC_E_ARG, "pfac_expand: null count_all");
+    *count_all = 0;
+    if (!a) return fail(PFAC_E_ARG, "pfac_expand: null automaton");
+    if (capacity > 0 && !d_pos_all) return fail(PFAC_E_ARG, "pfac_expand: null d_pos_all");
+    const void *probe = capacity > 0 ? (const void *)d_pos_all : (const void *)d_pos;
+    if (!probe) return count == 0 ? PFAC_OK : fail(PFAC_E_ARG, "pfac_expand: null buffers");
+    const int dev = device_of(probe);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_expand: buffers are not device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    void *scratch = nullptr;
+    cudaError_t ce = cudaMallocAsync(&scratch, expand_workspace_bytes() + 16, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "pfac_expand: scratch allocation");
+    uint64_t *d_counts = reinterpret_cast<uint64_t *>(scratch);  // [0] = count in, [1] = count out
+    void *ws = d_counts + 2;
+    uint64_t h[2] = {count, 0};
+    int rc = PFAC_OK;
+    ce = cudaMemcpyAsync(d_counts, h, 8, cudaMemcpyHostToDevice, st);
+    if (!ce) {
+        rc = pfac_expand_async(a, d_pos, d_pid, d_counts, count, d_pos_all, d_pid_all, capacity, d_counts + 1, ws,
+                               stream);
+        if (!rc) ce = cudaMemcpyAsync(&h[1], d_counts + 1, 8, cudaMemcpyDeviceToHost, st);
+        if (!rc && !ce) ce = cudaStreamSynchronize(st);
+    }
+    cudaFreeAsync(scratch, st);
+    if (ce) return cuda_fail(ce, "pfac_expand");
+    if (rc) return rc;
+    *count_all = h[1];
+    if (h[1] > capacity) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "pfac_expand: %llu occurrences > capacity %llu", (unsigned long long)h[1],
                  (unsigned long long)capacity);
         return fail(PFAC_E_CAPACITY, msg);
     }

@@ -105,6 +105,7 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
         a->table.assign((size_t)S * 4, 0);
         a->depth.assign(S, 0);
         a->F.assign(S, 0);
+        a->chain.assign(2 * ((size_t)k + 1), 0);
         std::vector<uint32_t> newid(S, 0);
         std::vector<uint32_t> order;  // insertion ids in BFS order
         order.reserve(S);
@@ -120,6 +121,11 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
                 a->table[(size_t)newid[u] * 4 + c] = id;
                 a->depth[id] = a->depth[newid[u]] + 1;
                 a->F[id] = fin[v] ? fin[v] : a->F[newid[u]];
+                if (fin[v]) {  // prefix chain: the longest pattern that is a proper prefix of this one
+                    const uint32_t q = a->F[newid[u]];  // shallower, so its chain length is known
+                    a->chain[2 * (size_t)id] = q;
+                    a->chain[2 * (size_t)id + 1] = 1 + a->chain[2 * (size_t)q + 1];
+                }
                 order.push_back(v);
             }
         }

@@ -95,6 +95,7 @@ struct DeviceImage {
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
     uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
     uint32_t *d_FB = nullptr;                             // K2 > 0: K1-mer filter bitmap
+    const uint32_t *d_chain = nullptr;                    // 2*(k+1): (prefix parent, chain length)
     size_t l2_persist_bytes = 0;                          // access-policy window from d_base (0 = none)
     ScanCtx *scan = nullptr;                              // created by the first pfac_scan_host
 };
@@ -109,6 +110,8 @@ struct pfac_automaton {
     std::vector<uint32_t> table;  // canonical S*4, columns A,C,G,T
     std::vector<uint32_t> depth;  // canonical depth of each state
     std::vector<uint32_t> F;      // canonical: deepest final on the root path (pattern id) or 0
+    std::vector<uint32_t> chain;  // 2*(k+1): [2p] = longest pattern that is a proper prefix of p
+                                  // (0 = none), [2p+1] = patterns on p's prefix chain incl. p
     pfac::HostImage host_image;   // derived once at build
     std::mutex mu;                // guards images
     std::vector<pfac::DeviceImage *> images;
@@ -136,4 +139,8 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
+int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
+                  const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,
+                  uint64_t capacity, uint64_t *d_count_all, void *d_workspace, void *stream);
+uint64_t expand_workspace_bytes();
 }  // namespace pfac

@@ -149,3 +149,19 @@ def test_large_config_builds():
     a = Automaton(P)
     assert a.num_patterns == 1000 and a.max_len == 20
     assert 15000 < a.num_states < 17000  # SURVEY Appendix A estimate 15 818
+
+
+def test_prefix_chain_definition():
+    """pfac_prefix_chain: [p] = longest pattern that is a proper prefix of p, length = patterns that are
+    prefixes of p (p included) -- by direct string comparison."""
+    import random
+    rng = random.Random(5)
+    for trial in range(50):
+        k = rng.randint(1, 60)
+        pats = list({"".join(rng.choice("AC") for _ in range(rng.randint(1, 9))).encode() for _ in range(k)})
+        ch = Automaton(pats).prefix_chain()
+        assert ch[0].tolist() == [0, 0]
+        for i, p in enumerate(pats, start=1):
+            pre = [j for j, q in enumerate(pats, start=1) if len(q) < len(p) and p.startswith(q)]
+            parent = max(pre, key=lambda j: len(pats[j - 1])) if pre else 0
+            assert ch[i].tolist() == [parent, len(pre) + 1], (p, pats)

@@ -145,6 +145,36 @@ def test_expand_longest_equals_classic_ac():
         assert expand(out, P) == ClassicAC(P).occurrences(t)
 
 
+def test_match_all_equals_classic_ac_and_bruteforce():
+    """Oracle.match_all (every final the walk passes) == classic AC occurrences == brute force, as a list
+    ordered by position then length."""
+    rng = random.Random(13)
+    for trial in range(300):
+        P = _random_set(rng, rng.randint(1, 40), 1, rng.choice([3, 8, 20]))
+        t = bytearray("".join(rng.choice("ACGTN") for _ in range(rng.randint(0, 1500))).encode())
+        for _ in range(rng.randint(0, 20)):
+            if t:
+                p = rng.choice(P)
+                i = rng.randrange(len(t))
+                t[i:i + len(p)] = p
+        t = bytes(t)
+        pos, pid = Oracle(P).match_all(t)
+        got = list(zip(pos.tolist(), pid.tolist()))
+        exp = sorted(all_occurrences(P, t), key=lambda x: (x[0], len(P[x[1] - 1])))
+        assert got == exp
+        assert set(got) == ClassicAC(P).occurrences(t)
+
+
+def test_match_all_nested_closed_form():
+    """Nested family A^1..A^m over a poly-A run of length R then a non-A: position i has the
+    min(m, R-i) occurrences A^1..A^min(m, R-i), in that order."""
+    m, R = 7, 30
+    P = [b"A" * L for L in range(1, m + 1)]
+    pos, pid = Oracle(P).match_all(b"A" * R + b"C")
+    exp = [(i, L) for i in range(R) for L in range(1, min(m, R - i) + 1)]
+    assert list(zip(pos.tolist(), pid.tolist())) == exp
+
+
 # --------------------------------------------------------------------------- closed forms
 @pytest.mark.parametrize("k", [1, 2, 3, 5])
 def test_all_kmers_closed_form(k):
