@@ -250,7 +250,15 @@ def run_pfac(args):
     stream = torch.cuda.current_stream(dev)
     fused = args.path == "fused"
     graph_error = None
-    kernels_per_step = 2 if fused else 3
+    kernels_per_step = (2 if fused else 3) + (1 if args.all_matches else 0)
+    if args.all_matches:  # every occurrence: size the output from a probe
+        ws_e = torch.empty(P.expand_workspace_bytes(), dtype=torch.uint8, device=dev)
+        count_all = torch.zeros(1, dtype=torch.int64, device=dev)
+        P.match_compact_async(a, packed, n_own, n_avail, out, pos, pid, count, ws, pos_base=sh.start, inv=inv)
+        P.expand_async(a, pos, pid, count, pos[:0], pid[:0], count_all, ws_e)
+        cap_all = int(count_all.item()) + 1024
+        pos_all = torch.empty(cap_all, dtype=torch.int64, device=dev)
+        pid_all = torch.empty(cap_all, dtype=torch.int32, device=dev)
 
     def step(ev=None, st=None):
         st = stream if st is None else st
@@ -275,6 +283,10 @@ def run_pfac(args):
             P.compact_async(out, pos, pid, count, ws, pos_base=sh.start, k=len(pats), stream=st)
             if ev is not None:
                 ev[3].record(st)
+        if args.all_matches:
+            P.expand_async(a, pos, pid, count, pos_all, pid_all, count_all, ws_e, stream=st)
+        if ev is not None:
+            ev[4].record(st)
         if world > 1:
             m = int(count.item())
             gather_matches(pos, pid, min(m, cap), dst=0)
@@ -289,7 +301,7 @@ def run_pfac(args):
     assert m_final <= cap
 
     # per-kernel times: K steps with events between the C-ABI calls (also the timed pass without graphs)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
 
@@ -326,7 +338,7 @@ def run_pfac(args):
             graph = None
             graph_error = repr(ex)[:200]
     kt_ms = timed(event_steps)
-    kt = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evs])  # pack, match, compact
+    kt = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs])  # pack, match, compact, expand
     if graph is not None:
         clocks = ClockSampler(local)
         t_ms = timed(lambda: [graph.replay() for _ in range(args.steps)])
@@ -344,7 +356,7 @@ def run_pfac(args):
     value = n_total / (ms_per_step * 1e-3) / 1e9
 
     hbm, hbm_src = peaks()
-    pack_ms, match_ms, compact_ms = (float(x) for x in kt.mean(axis=0))
+    pack_ms, match_ms, compact_ms, expand_ms = (float(x) for x in kt.mean(axis=0))
     if fused:
         compact_ms = 0.0  # inside the fused kernel
     match_bpb = MATCH_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
@@ -410,6 +422,7 @@ def run_pfac(args):
             "cuda_graph": graph is not None, **({"cuda_graph_error": graph_error} if graph_error else {}),
             "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,
                            "compact": None if fused else compact_ms,
+                           **({"expand": expand_ms, "occurrences": int(count_all.item())} if args.all_matches else {}),
                            "pack_frac": pack_bpb * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
                            "compact_frac": (COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm
                                             if compact_ms > 0 else None)},
@@ -442,6 +455,8 @@ def main():
     ap.add_argument("--bases-per-rank", dest="n", type=int, default=None, help="override bases per rank (testing)")
     ap.add_argument("--barriers", type=int, default=None, metavar="LINE",
                     help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")
+    ap.add_argument("--all-matches", action="store_true",
+                    help="add the all-occurrence expansion (pfac_expand_async) to the timed step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -62,9 +62,10 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     // covers the J2 prefix.
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t bJ2 = al(h.J2.size() * 4), bT = al(h.T.size()), bF = al(h.F.size()), bJ = al(h.J.size()),
-                 bFB = al(h.FB.size() * 4), bC = al(a->chain.size() * 4);
+                 bFB = al(h.FB.size() * 4), bC = al(a->prefix_dev.size() * 4),
+                 bCF = al(a->prefix_flat.size() * 4);
     cudaError_t e = cudaSetDevice(device);
-    if (e == cudaSuccess) e = cudaMalloc(&im->d_base, bJ2 + bT + bF + bJ + bFB + bC);
+    if (e == cudaSuccess) e = cudaMalloc(&im->d_base, bJ2 + bT + bF + bJ + bFB + bC + bCF);
     if (e == cudaSuccess) {
         uint8_t *b = reinterpret_cast<uint8_t *>(im->d_base);
         im->d_J2 = h.K2 ? reinterpret_cast<uint32_t *>(b) : nullptr;
@@ -72,9 +73,13 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
         im->d_F = b + bJ2 + bT;
         im->d_J = b + bJ2 + bT + bF;
         im->d_FB = h.K2 ? reinterpret_cast<uint32_t *>(b + bJ2 + bT + bF + bJ) : nullptr;
-        im->d_chain = reinterpret_cast<const uint32_t *>(b + bJ2 + bT + bF + bJ + bFB);
-        e = cudaMemcpy(const_cast<uint32_t *>(im->d_chain), a->chain.data(), a->chain.size() * 4,
-                       cudaMemcpyHostToDevice);
+        uint32_t *dp = reinterpret_cast<uint32_t *>(b + bJ2 + bT + bF + bJ + bFB);
+        uint32_t *dpf = reinterpret_cast<uint32_t *>(b + bJ2 + bT + bF + bJ + bFB + bC);
+        im->d_prefix = dp;
+        im->d_prefix_flat = dpf;
+        e = cudaMemcpy(dp, a->prefix_dev.data(), a->prefix_dev.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(dpf, a->prefix_flat.data(), a->prefix_flat.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess)
             e = cudaMemcpy(im->d_T, h.T.data(), h.T.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
@@ -527,7 +532,7 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     return PFAC_OK;
 }
 
-const uint32_t *pfac_prefix_chain(const pfac_automaton *a) { return a ? a->chain.data() : nullptr; }
+const uint32_t *pfac_prefix_chain(const pfac_automaton *a) { return a ? a->prefix.data() : nullptr; }
 
 uint64_t pfac_expand_workspace_bytes(void) { return expand_workspace_bytes(); }
 

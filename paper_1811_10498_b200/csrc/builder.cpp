@@ -10,6 +10,7 @@
 //  4. Derive the device image: the same automaton renumbered chain-major, its
 //     unary runs stored as "chain rows" (up to 16 forced bases compared at once), the per-state
 //     answer F, and a jump table J over all K-mers that performs the first K steps of every walk.
+#include <algorithm>
 #include <cstdio>
 
 #include "../../include/pfac.h"
@@ -105,8 +106,10 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
         a->table.assign((size_t)S * 4, 0);
         a->depth.assign(S, 0);
         a->F.assign(S, 0);
-        a->chain.assign(2 * ((size_t)k + 1), 0);
+        a->prefix.assign(2 * ((size_t)k + 1), 0);
         std::vector<uint32_t> newid(S, 0);
+        std::vector<uint32_t> fin_order;  // pattern ids in BFS (non-decreasing length) order
+        fin_order.reserve(k);
         std::vector<uint32_t> order;  // insertion ids in BFS order
         order.reserve(S);
         order.push_back(0);
@@ -123,11 +126,36 @@ int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, p
                 a->F[id] = fin[v] ? fin[v] : a->F[newid[u]];
                 if (fin[v]) {  // prefix chain: the longest pattern that is a proper prefix of this one
                     const uint32_t q = a->F[newid[u]];  // shallower, so its chain length is known
-                    a->chain[2 * (size_t)id] = q;
-                    a->chain[2 * (size_t)id + 1] = 1 + a->chain[2 * (size_t)q + 1];
+                    a->prefix[2 * (size_t)id] = q;
+                    a->prefix[2 * (size_t)id + 1] = 1 + a->prefix[2 * (size_t)q + 1];
+                    fin_order.push_back(id);
                 }
                 order.push_back(v);
             }
+        }
+        // Flattened prefix chains for the expand kernel: pattern p's chain, shortest first, at
+        // prefix_flat[base(p) .. base(p) + len(p)); len(p) <= |p|, so the array is at most the total
+        // pattern length.  Filled in BFS order so that a prefix's chain is ready before it is copied.
+        a->prefix_dev.assign(4 * ((size_t)k + 1), 0);
+        uint64_t flat = 0;
+        for (uint32_t p = 1; p <= k; ++p) {
+            const uint32_t len = a->prefix[2 * (size_t)p + 1];
+            a->prefix_dev[4 * (size_t)p + 0] = len;
+            a->prefix_dev[4 * (size_t)p + 1] = a->prefix[2 * (size_t)p];
+            a->prefix_dev[4 * (size_t)p + 2] = (uint32_t)flat;
+            a->prefix_dev[4 * (size_t)p + 3] = (uint32_t)(flat >> 32);
+            flat += len;
+        }
+        a->prefix_flat.assign(flat ? flat : 1, 0);
+        for (uint32_t p : fin_order) {
+            const size_t b = a->prefix_dev[4 * (size_t)p + 2] | ((uint64_t)a->prefix_dev[4 * (size_t)p + 3] << 32);
+            const uint32_t len = a->prefix_dev[4 * (size_t)p], q = a->prefix[2 * (size_t)p];
+            if (q) {
+                const size_t bq = a->prefix_dev[4 * (size_t)q + 2] | ((uint64_t)a->prefix_dev[4 * (size_t)q + 3] << 32);
+                std::copy(a->prefix_flat.begin() + bq, a->prefix_flat.begin() + bq + (len - 1),
+                          a->prefix_flat.begin() + b);
+            }
+            a->prefix_flat[b + len - 1] = p;
         }
     } catch (...) {
         delete a;

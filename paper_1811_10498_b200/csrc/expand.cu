@@ -11,9 +11,12 @@
 // One persistent cooperative grid; each warp owns a contiguous run of input entries:
 //   pass 1: the warp sums the chain lengths of its entries;
 //   grid_prefix: ordered offsets across warps and CTAs (compact_common.cuh);
-//   pass 2: 32 entries per round, a warp scan of their chain lengths gives each lane its output
-//           offset, and the lane writes its chain shortest-first (a chain is followed longest-first,
-//           so element t goes to offset + len - 1 - t).
+//   pass 2: 32 entries per round; their outputs form one contiguous range, which the lanes fill
+//           with stride 32 (coalesced 8-byte and 4-byte stores): output r of the round belongs to
+//           the entry whose inclusive chain-length scan first exceeds r (a 5-step shuffle search),
+//           and its pattern id is element t of that entry's flattened chain (prefix_flat, shortest
+//           first, built on the host).  Long chains (cfg5: ~80 per match) and short ones (1) both
+//           keep every lane busy.
 // HBM-bound on the output: 12 B per occurrence written, 12 B per input entry read.
 #include <cuda_runtime.h>
 
@@ -31,7 +34,8 @@ struct ExpandArgs {
     const uint32_t *pid;
     const uint64_t *count;  // device: entries in the input list (read at run time)
     uint64_t in_cap;        // entries readable from pos/pid
-    const uint2 *chain;     // k+1 (prefix parent, chain length)
+    const uint4 *prefix;    // k+1: (chain length, parent, flat base lo, hi)
+    const uint32_t *flat;   // chains, shortest first
     uint32_t k;
     uint64_t *pos_all;
     uint32_t *pid_all;
@@ -47,19 +51,25 @@ __global__ void __launch_bounds__(kEWarps * 32) expand_kernel(ExpandArgs a) {
     const uint64_t nw = (uint64_t)gridDim.x * kEWarps, gw = (uint64_t)blockIdx.x * kEWarps + warp;
     const uint64_t per = ((m + nw - 1) / nw + 31) & ~31ull;
     const uint64_t lo = gw * per < m ? gw * per : m, hi = lo + per < m ? lo + per : m;
-    auto len_of = [&](uint32_t p) -> uint32_t { return p && p <= a.k ? __ldg(&a.chain[p].y) : 0u; };
     uint64_t wcount = 0;
-    for (uint64_t j = lo + lane; j < hi; j += 32) wcount += len_of(__ldg(a.pid + j));
+    for (uint64_t j = lo + lane; j < hi; j += 32) {
+        const uint32_t p = __ldg(a.pid + j);
+        wcount += p && p <= a.k ? __ldg(&a.prefix[p].x) : 0u;
+    }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) wcount += __shfl_xor_sync(~0u, wcount, d);
     uint64_t run = grid_prefix<kEWarps>(wcount, a.counts, a.count_all, s_wcount, s_woff);
     for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
         const uint64_t j = j0 + lane;
-        uint32_t p = 0, c = 0;
-        uint64_t x = 0;
+        uint32_t c = 0;
+        uint64_t x = 0, base = 0;
         if (j < hi) {
-            p = __ldg(a.pid + j);
-            c = len_of(p);
+            const uint32_t p = __ldg(a.pid + j);
+            if (p && p <= a.k) {
+                const uint4 e = __ldg(&a.prefix[p]);
+                c = e.x;
+                base = e.z | ((uint64_t)e.w << 32);
+            }
             x = __ldg(a.pos + j);
         }
         uint32_t incl = c;
@@ -68,16 +78,25 @@ __global__ void __launch_bounds__(kEWarps * 32) expand_kernel(ExpandArgs a) {
             const uint32_t y = __shfl_up_sync(~0u, incl, d);
             if (lane >= (uint32_t)d) incl += y;
         }
-        const uint64_t off = run + incl - c;
-        for (uint32_t t = 0; t < c; ++t) {
-            const uint64_t r = off + c - 1 - t;
-            if (r < a.cap) {
-                a.pos_all[r] = x;
-                a.pid_all[r] = p;
+        const uint32_t total = __shfl_sync(~0u, incl, 31);
+        const uint64_t first = base - (incl - c);  // flat index of output (incl - c) + t, per entry
+        for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+            const uint32_t r = r0 + lane;
+            // entry e = the first lane whose inclusive scan exceeds r
+            uint32_t e = 0;
+#pragma unroll
+            for (uint32_t step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(~0u, incl, e + step - 1);
+                if (v <= r) e += step;
             }
-            p = __ldg(&a.chain[p].x);
+            const uint64_t xe = __shfl_sync(~0u, x, e), fe = __shfl_sync(~0u, first, e);
+            const uint64_t o = run + r;
+            if (r < total && o < a.cap) {
+                a.pos_all[o] = xe;
+                a.pid_all[o] = __ldg(a.flat + fe + r);
+            }
         }
-        run += __shfl_sync(~0u, incl, 31);
+        run += total;
     }
 }
 
@@ -100,7 +119,8 @@ int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, con
     a.pid = d_pid;
     a.count = d_count;
     a.in_cap = in_capacity;
-    a.chain = reinterpret_cast<const uint2 *>(img.d_chain);
+    a.prefix = reinterpret_cast<const uint4 *>(img.d_prefix);
+    a.flat = img.d_prefix_flat;
     a.k = k;
     a.pos_all = d_pos_all;
     a.pid_all = d_pid_all;

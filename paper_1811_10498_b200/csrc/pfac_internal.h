@@ -95,7 +95,8 @@ struct DeviceImage {
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
     uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
     uint32_t *d_FB = nullptr;                             // K2 > 0: K1-mer filter bitmap
-    const uint32_t *d_chain = nullptr;                    // 2*(k+1): (prefix parent, chain length)
+    const uint32_t *d_prefix = nullptr;                   // prefix_dev (uint4 per pattern)
+    const uint32_t *d_prefix_flat = nullptr;              // prefix_flat
     size_t l2_persist_bytes = 0;                          // access-policy window from d_base (0 = none)
     ScanCtx *scan = nullptr;                              // created by the first pfac_scan_host
 };
@@ -110,8 +111,10 @@ struct pfac_automaton {
     std::vector<uint32_t> table;  // canonical S*4, columns A,C,G,T
     std::vector<uint32_t> depth;  // canonical depth of each state
     std::vector<uint32_t> F;      // canonical: deepest final on the root path (pattern id) or 0
-    std::vector<uint32_t> chain;  // 2*(k+1): [2p] = longest pattern that is a proper prefix of p
-                                  // (0 = none), [2p+1] = patterns on p's prefix chain incl. p
+    std::vector<uint32_t> prefix;      // 2*(k+1): [2p] = longest pattern that is a proper prefix of p
+                                       // (0 = none), [2p+1] = patterns on p's prefix chain incl. p
+    std::vector<uint32_t> prefix_dev;  // 4*(k+1): (chain length, parent, flat base lo, hi) per pattern
+    std::vector<uint32_t> prefix_flat; // every pattern's chain, shortest first, at its flat base
     pfac::HostImage host_image;   // derived once at build
     std::mutex mu;                // guards images
     std::vector<pfac::DeviceImage *> images;
