@@ -35,6 +35,16 @@ namespace pfac {
 #ifndef PFAC_MT
 #define PFAC_MT 896
 #endif
+// Ablation knobs (report-only builds, scripts/ablations.sh):
+//   PFAC_TEXT_DIRECT=1: the walk reads the packed text straight from global memory (L1/L2) instead
+//     of the per-warp TMA-staged shared-memory slices (the paper's "text in shared memory" question,
+//     PAPER.md:327-330).  Reads may touch up to 16 bytes past the packed buffer (the bench's caching
+//     allocator rounds allocations up), so it is not a product setting.
+//   PFAC_WINDOW_MAX=W: at most W transition-table rows staged in shared memory (0: every row through
+//     L2 with ld.global.nc -- the paper's table-in-texture/global question).
+#ifndef PFAC_TEXT_DIRECT
+#define PFAC_TEXT_DIRECT 0
+#endif
 #ifndef PFAC_PH1_UNROLL
 #define PFAC_PH1_UNROLL 1
 #endif
@@ -213,7 +223,9 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     const uint64_t s_end = CONTIG ? (s_first + p.slices_per_warp < p.nslices ? s_first + p.slices_per_warp : p.nslices)
                                   : p.nslices;
     const uint64_t s_stride = CONTIG ? 1 : TW;
+    constexpr bool DIRECT = PFAC_TEXT_DIRECT && !BAR;
     auto issue = [&](uint64_t sl, uint32_t *dst, uint64_t *b) {
+        if constexpr (DIRECT) return;
         const uint64_t w0 = sl * (kSlice / 16);
         const uint64_t left = p.avail_words - w0;
         const uint32_t nw = left < p.slice_words ? (uint32_t)left : p.slice_words;
@@ -260,8 +272,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             for (uint32_t w = lane; w < kBmWords; w += 32) bm[w] = 0;
             __syncwarp();
         }
-        mbar_wait(&bar[buf], (it >> 1) & 1);
-        const uint32_t *txt = buf ? txt1 : txt0;
+        if constexpr (!DIRECT) mbar_wait(&bar[buf], (it >> 1) & 1);
+        const uint32_t *txt = DIRECT ? p.packed + sl * (kSlice / 16) : (buf ? txt1 : txt0);
         const uint16_t *inv = buf ? inv1 : inv0;
         (void)inv;
         const uint64_t base = sl * kSlice;
@@ -501,10 +513,16 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
         if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
-            uint32_t any = 0;
-            for (uint32_t w = lane; w < kBmWords; w += 32) any |= bm[w];
+            uint32_t cnt = 0;
+            for (uint32_t w = lane; w < kBmWords; w += 32) cnt += __popc(bm[w]);
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
+            // Once the staging area cannot hold them, only count: the warp re-reads its out[] range
+            // after the grid prefix anyway (dense outputs, e.g. cfg5).
+            const bool stage = cnt != 0 && wcount + cnt <= p.c.stg;
+            if (!stage) wcount += cnt;
 #pragma unroll 1
-            for (uint32_t w0 = 0; w0 < kBmWords && __any_sync(~0u, any); w0 += 32) {
+            for (uint32_t w0 = 0; stage && w0 < kBmWords; w0 += 32) {
                 uint32_t w = bm[w0 + lane];
                 const uint32_t c = __popc(w);
                 uint32_t incl = c;
@@ -559,6 +577,10 @@ static void dev_props(int device, int &sms, int &optin) {
     optin = o;
 }
 
+#ifndef PFAC_WINDOW_MIN_SHARE
+#define PFAC_WINDOW_MIN_SHARE 4
+#endif
+constexpr uint32_t kWindowMinShare = PFAC_WINDOW_MIN_SHARE;  // keep a row window only if rows <= this x window
 constexpr size_t kStaticSmemReserve = 1024;  // the fused kernel's static shared arrays (grid_prefix)
 
 static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
@@ -575,14 +597,26 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     const size_t table = h.K2 ? (size_t)kFBBytes : ((size_t)1 << (2 * h.K)) * pl.cell;
     const size_t fixed = match_smem(table, pl.cell, 0, pl.slice_words) + kStaticSmemReserve;
     const size_t budget = (size_t)optin > fixed ? (size_t)optin - fixed : 0;
-    const uint32_t w = (uint32_t)(budget / (5 * pl.cell)) & ~7u;
+    uint32_t w = (uint32_t)(budget / (5 * pl.cell)) & ~7u;
+#ifdef PFAC_WINDOW_MAX
+    if (w > (uint32_t)(PFAC_WINDOW_MAX)) w = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
+#endif
+    // A window that holds only a small share of the rows (huge uint32 automata, cfg4: 5.4 M states vs
+    // ~3 k rows) costs more than it saves: lanes split between the shared and the global row path,
+    // and its shared memory is better left to L1, which then caches the hot rows itself
+    // (profiles/r01_ablations.md: window0 is 18% faster on cfg4, neutral elsewhere).
+    if (w < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * w) w = 0;
     pl.all_smem = w >= h.rows;
     pl.window = pl.all_smem ? h.rows : w;
     pl.smem = match_smem(table, pl.cell, pl.window, pl.slice_words);
     // barrier-mode variant (BAR): per-warp barrier bits take room from the row window
     const size_t fixed_b = match_smem(table, pl.cell, 0, pl.slice_words, true) + kStaticSmemReserve;
     const size_t budget_b = (size_t)optin > fixed_b ? (size_t)optin - fixed_b : 0;
-    const uint32_t wb = (uint32_t)(budget_b / (5 * pl.cell)) & ~7u;
+    uint32_t wb = (uint32_t)(budget_b / (5 * pl.cell)) & ~7u;
+    if (wb < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wb) wb = 0;
+#ifdef PFAC_WINDOW_MAX
+    if (wb > (uint32_t)(PFAC_WINDOW_MAX)) wb = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
+#endif
     pl.all_smem_bar = wb >= h.rows;
     pl.window_bar = pl.all_smem_bar ? h.rows : wb;
     pl.smem_bar = match_smem(table, pl.cell, pl.window_bar, pl.slice_words, true);

@@ -1,0 +1,27 @@
+"""Build the ablation variants of libpfac into paper_1811_10498_b200/_lib/alt/.
+
+Each variant is the product library with one PFAC_* knob flipped; scripts/ablations.sh benches them.
+"""
+import concurrent.futures as cf
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1811_10498_b200 import _build  # noqa: E402
+
+ALT = os.path.join(os.path.dirname(_build.LIB), "alt")
+VARIANTS = {
+    "text_direct": ["PFAC_TEXT_DIRECT=1"],   # text read from global (L1/L2), no TMA staging
+    "window0": ["PFAC_WINDOW_MAX=0"],        # no transition-table rows in shared memory
+    "jtable": ["PFAC_FB16=0"],               # uint16 images: 4^8 jump table instead of filter + J2
+    "nopersist": ["PFAC_NO_PERSIST"],        # no L2 access-policy window over J2
+}
+
+if __name__ == "__main__":
+    os.makedirs(ALT, exist_ok=True)
+    names = sys.argv[1:] or list(VARIANTS)
+    with cf.ThreadPoolExecutor(4) as ex:
+        futs = {ex.submit(_build.build, out=os.path.join(ALT, f"libpfac_{n}.so"), defines=VARIANTS[n]): n
+                for n in names}
+        for f in cf.as_completed(futs):
+            print(futs[f], "->", f.result())
