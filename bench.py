@@ -248,7 +248,10 @@ def run_pfac(args):
     pos = torch.empty(cap, dtype=torch.int64, device=dev)
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    fused = args.path == "fused"
+    fused = args.path in ("fused", "list")
+    list_only = args.path == "list"
+    if list_only:  # the list without the dense out[] (scratch workspace)
+        ws = torch.empty(P.match_list_workspace_bytes(n_own), dtype=torch.uint8, device=dev)
     graph_error = None
     kernels_per_step = (2 if fused else 3) + (1 if args.all_matches else 0)
     if args.all_matches:  # every occurrence: size the output from a probe
@@ -267,7 +270,13 @@ def run_pfac(args):
         pack(st)
         if ev is not None:
             ev[1].record(st)
-        if fused:  # match + compact in one kernel
+        if list_only:
+            P.match_list_async(a, packed, n_own, n_avail, pos, pid, count, ws, pos_base=sh.start, inv=inv,
+                               stream=st)
+            if ev is not None:
+                ev[2].record(st)
+                ev[3].record(st)
+        elif fused:  # match + compact in one kernel
             P.match_compact_async(a, packed, n_own, n_avail, out, pos, pid, count, ws, pos_base=sh.start,
                                   stream=st, inv=inv)
             if ev is not None:
@@ -360,6 +369,8 @@ def run_pfac(args):
     if fused:
         compact_ms = 0.0  # inside the fused kernel
     match_bpb = MATCH_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
+    if list_only:  # packed text read + 12 B per match written (no out[])
+        match_bpb = 0.25 + (BARRIER_BYTES_PER_BASE if bars else 0.0) + 12.0 * m_final / max(1, n_own)
     pack_bpb = PACK_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
     match_gbs = match_bpb * n_own / (match_ms * 1e-3) / 1e9
     traffic = profiled_traffic(args.config, args.path) if args.n is None and not bars else None
@@ -395,7 +406,11 @@ def run_pfac(args):
     if rank == 0:
         from oracle import Oracle
         w = min(n_own, 200_000)
-        assert (out[:w].cpu().numpy() == Oracle(pats).match(text, 0, w, n=n_avail)).all()
+        if list_only:
+            ep, ei = Oracle(pats).match_list(text, 0, w, n=n_avail)
+            assert (pos[:len(ep)].cpu().numpy() == ep.astype(np.int64) + sh.start).all()
+        else:
+            assert (out[:w].cpu().numpy() == Oracle(pats).match(text, 0, w, n=n_avail)).all()
         if world == 1 and not args.no_cpu_baseline:
             m, dt, _ = oracle_sample(pats, text, n_own, args.cpu_seconds)
             cpu = {"value": m / dt / 1e9, "unit": "Gbases/s", "cores": 1, "kind": "oracle",
@@ -415,7 +430,8 @@ def run_pfac(args):
                        "matches_per_step": m_final, "image": a.image_info(local)},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
-                         "kernel": ("match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel")
+                         "kernel": ("match_kernel<FUSE=1, list-only>" if list_only else
+                                    "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel")
                          + ("<BAR=1>" if bars else ""),
                          "algorithmic_bytes_per_launch": match_bpb * n_own, "peak_source": hbm_src},
             "path": args.path,
@@ -450,8 +466,9 @@ def main():
                     help="launch the step's kernels directly instead of replaying one captured CUDA graph")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="process group for N>1 (gloo only to test the multi-rank flow on one GPU)")
-    ap.add_argument("--path", choices=["fused", "separate"], default="fused",
-                    help="fused: pack -> match+compact kernel; separate: pack -> match -> compact")
+    ap.add_argument("--path", choices=["fused", "separate", "list"], default="fused",
+                    help="fused: pack -> match+compact kernel; separate: pack -> match -> compact; "
+                         "list: pack -> list-only match (no dense out[])")
     ap.add_argument("--bases-per-rank", dest="n", type=int, default=None, help="override bases per rank (testing)")
     ap.add_argument("--barriers", type=int, default=None, metavar="LINE",
                     help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")

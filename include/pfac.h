@@ -162,6 +162,22 @@ int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d
                                       uint64_t *d_hist, void *d_workspace, void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * List-only match (second half): the match list of
+ * pfac_match_compact_async without the dense out[] array -- the paper's output is the dense array
+ * (PAPER.md:207); when only the occurrences are wanted, skipping it cuts the kernel's HBM traffic
+ * from 4.25 to ~0.25 B/base (+12 B per match).  d_inv: barrier masks as for
+ * pfac_match_barriers_async, or null.  d_workspace holds pfac_match_list_workspace_bytes(n_own)
+ * bytes, 16-byte aligned (any content; it includes an n_own-int32 scratch written only at match
+ * positions).  Images without the filter (PFAC_FB16=0 builds) return PFAC_E_CUDA.  Asynchronous
+ * (a cooperative launch).
+ */
+uint64_t pfac_match_list_workspace_bytes(uint64_t n_own);
+int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv,
+                          uint64_t n_own, uint64_t n_avail, uint64_t pos_base, uint64_t *d_pos,
+                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist,
+                          void *d_workspace, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * End to end over HOST memory (the call a user with a text in RAM makes): the match list
  * {(pos_base + i, out[i]) : out[i] != 0, i < n_own} of the ASCII text h_text[0..n_avail) (walks
  * read up to n_avail >= n_own: a shard and its halo) on CUDA device `device`.  The text is streamed

@@ -63,6 +63,11 @@ _SIGS = {
     "pfac_expand": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                    ctypes.c_void_p]),
+    "pfac_match_list_workspace_bytes": (ctypes.c_uint64, [ctypes.c_uint64]),
+    "pfac_match_list_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p]),
     "pfac_image_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "pfac_scan_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
@@ -80,7 +85,12 @@ def lib() -> ctypes.CDLL:
             _build.build()
         L = ctypes.CDLL(path)
         for name, (res, args) in _SIGS.items():
-            f = getattr(L, name)
+            try:
+                f = getattr(L, name)
+            except AttributeError:
+                if os.environ.get("PFAC_LIB"):  # A/B runs may load an older build lacking newer entry points
+                    continue
+                raise
             f.restype = res
             f.argtypes = args
         _lib = L
@@ -349,3 +359,16 @@ def expand(a: Automaton, pos, pid, capacity: int | None = None, stream=None):
         _check(rc)
         t = int(c.value)
         return pa[:t], pi[:t], t
+
+
+def match_list_workspace_bytes(n_own: int) -> int:
+    return int(lib().pfac_match_list_workspace_bytes(n_own))
+
+
+def match_list_async(a: Automaton, packed, n_own: int, n_avail: int, pos, pid, count, workspace, pos_base: int = 0,
+                     hist=None, inv=None, stream=None):
+    """pfac_match_list_async: the ordered match list without the dense out[] (count: 1-element int64 CUDA
+    tensor; workspace: match_list_workspace_bytes(n_own) bytes)."""
+    _check(lib().pfac_match_list_async(a.handle, _ptr(packed), _ptr(inv), n_own, n_avail, pos_base, _ptr(pos),
+                                       _ptr(pid), pos.numel(), _ptr(count), _ptr(hist), _ptr(workspace),
+                                       _stream(stream, count.device)))

@@ -286,6 +286,36 @@ int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d
     return e ? cuda_fail(e, "pfac_match_compact_async") : PFAC_OK;
 }
 
+uint64_t pfac_match_list_workspace_bytes(uint64_t n_own) { return compact_workspace_bytes(n_own) + n_own * 4 + 16; }
+
+int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv, uint64_t n_own,
+                          uint64_t n_avail, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                          uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match_list_async: null automaton");
+    if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_list_async: n_avail < n_own");
+    if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_match_list_async: null d_count / d_workspace");
+    if (capacity > 0 && (!d_pos || !d_pid)) return fail(PFAC_E_ARG, "pfac_match_list_async: null d_pos / d_pid");
+    if (n_own > 0 && !d_packed) return fail(PFAC_E_ARG, "pfac_match_list_async: null d_packed");
+    if (n_own > 0 && (!aligned16(d_packed) || !aligned16(d_workspace) || (d_inv && !aligned16(d_inv))))
+        return fail(PFAC_E_ARG, "pfac_match_list_async: d_packed, d_inv and d_workspace must be 16-byte aligned");
+    const int dev = device_of(d_count);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match_list_async: d_count is not device memory");
+    if (n_own == 0) {
+        cudaError_t e = cudaMemsetAsync(d_count, 0, 8, (cudaStream_t)stream);
+        return e ? cuda_fail(e, "pfac_match_list_async") : PFAC_OK;
+    }
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, dev, &im);
+    if (rc) return rc;
+    // the sparse out[] scratch sits after the compaction workspace: written only where a pattern
+    // matches, read back only there
+    int32_t *scratch = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(d_workspace) +
+                                                   ((compact_workspace_bytes(n_own) + 15) & ~15ull));
+    int e = launch_match_compact(*im, a->k, d_packed, d_inv, n_own, n_avail, scratch, pos_base, d_pos, d_pid, capacity,
+                                 d_count, d_hist, d_workspace, stream, true);
+    return e ? cuda_fail(e, "pfac_match_list_async") : PFAC_OK;
+}
+
 int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
                              int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
                              uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {

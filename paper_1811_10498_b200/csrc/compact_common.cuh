@@ -26,6 +26,7 @@ struct CompactArgs {
     uint32_t *stage_pid;
     uint64_t stg;         // staging entries per warp
     uint64_t chunk;       // ints per warp (multiple of kStep)
+    uint32_t *bitmap;     // fused kernel: match bitmaps of the slices its staging could not hold
 };
 
 __device__ __forceinline__ void load_step(const int32_t *out, uint64_t n, uint64_t b, uint32_t lane, uint4 (&v)[4]) {
@@ -45,15 +46,30 @@ __device__ __forceinline__ void load_step(const int32_t *out, uint64_t n, uint64
 
 // Streams [lo, hi) of out[] with one warp; emit(rank, position, value) for every nonzero entry in
 // position order, rank counted from wbase.  Returns the number of nonzero entries.
+// bits (nullable): a position-indexed bitmap (bit i%32 of word i/32); when given, only entries whose
+// bit is set count (the list-only kernel's out[] scratch holds values only there).  lo is a multiple of 32.
 template <typename Emit>
 __device__ __forceinline__ uint64_t warp_stream(const CompactArgs &a, uint64_t lo, uint64_t hi, uint64_t wbase,
-                                                Emit emit) {
+                                                Emit emit, const uint32_t *bits = nullptr) {
     const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1;
     uint64_t local = 0;
     uint4 v[4], vn[4];
     if (lo < hi) load_step(a.out, a.n, lo, lane, v);
     for (uint64_t b = lo; b < hi; b += kStep) {
         if (b + kStep < hi) load_step(a.out, a.n, b + kStep, lane, vn);
+        if (bits) {  // lane's 4 positions b + 128q + 4 lane .. +3: a nibble of word (b + 128q)/32 + lane/8
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t p0 = b + 128 * q + 4 * lane;
+                const uint32_t m = p0 < hi ? (ld_cg_u32(reinterpret_cast<const int32_t *>(bits + (p0 >> 5))) >>
+                                              (p0 & 31)) & 0xFu
+                                           : 0u;
+                v[q].x = m & 1 ? v[q].x : 0u;
+                v[q].y = m & 2 ? v[q].y : 0u;
+                v[q].z = m & 4 ? v[q].z : 0u;
+                v[q].w = m & 8 ? v[q].w : 0u;
+            }
+        }
         uint32_t any = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) any |= v[q].x | v[q].y | v[q].z | v[q].w;
@@ -126,6 +142,10 @@ __device__ __forceinline__ void put_match(const CompactArgs &a, uint64_t r, uint
     }
     if (a.hist && val <= a.k) atomicAdd(reinterpret_cast<unsigned long long *>(a.hist + val), 1ull);
 }
+
+// Workspace of the fused kernel's spilled slice bitmaps: one bit per position, whole slices
+// (a slice is <= 65536 positions), 16-byte multiple.
+inline uint64_t spill_bitmap_bytes(uint64_t n) { return (((n + 65536) / 32) * 4 + 15) & ~15ull; }
 
 inline uint64_t stage_entries(uint64_t n) {
     const uint64_t cap = kStageBytes / 12;

@@ -186,9 +186,10 @@ static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, b
            (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);                // BAR: the slice's barrier bits
 }
 
-template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false>
+template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
+    static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
@@ -262,7 +263,9 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     mbar_wait(tab_bar, 0);
 
     uint32_t it = 0;
-    uint64_t wcount = 0;  // fused: matches staged by this warp so far
+    uint64_t wcount = 0;   // fused: matches of this warp so far
+    uint32_t wstaged = 0;     // fused: of which staged (<= stg; the rest are streamed after the prefix)
+    uint32_t spill_rel = ~0u; // fused: first spilled slice, relative to s_first
     uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
     uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
     for (uint64_t sl = s_first; sl < s_end; sl += s_stride, ++it) {
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], le[k]);  // near the end / a barrier
                         else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, le[k]);
                         else res = g[k];
-                        out[l[k]] = (int32_t)res;
+                        if (!LIST || res) out[l[k]] = (int32_t)res;
                         if (FUSE && res) atomicOr(&bm[l[k] >> 5], 1u << (l[k] & 31));
                     }
                     qn -= take;
@@ -385,8 +388,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
                         m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
                     }
-                    st_stream_v4(out + l0, 0u, 0u, 0u, 0u);
-                    st_stream_v4(out + l0 + 4, 0u, 0u, 0u, 0u);
+                    if constexpr (!LIST) {
+                        st_stream_v4(out + l0, 0u, 0u, 0u, 0u);
+                        st_stream_v4(out + l0 + 4, 0u, 0u, 0u, 0u);
+                    }
                     am |= m << (r * kP);
                 } else {
                     uint32_t e[kP];
@@ -444,7 +449,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     m = ((fb & ~near) | (near & ~dead)) & 0xFFu;
                     m &= own;
                 }
-                if (l0 + kP <= lown) {
+                if (LIST) {
+                } else if (l0 + kP <= lown) {
                     st_stream_v4(out + l0, 0u, 0u, 0u, 0u);
                     st_stream_v4(out + l0 + 4, 0u, 0u, 0u, 0u);
                 } else {
@@ -513,48 +519,61 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
         if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
+            uint32_t any = 0;
+            for (uint32_t w = lane; w < kBmWords; w += 32) any |= bm[w];
             uint32_t cnt = 0;
-            for (uint32_t w = lane; w < kBmWords; w += 32) cnt += __popc(bm[w]);
+            if (__any_sync(~0u, any)) {  // most slices have no match (cfg2: 0.5 per slice)
+                for (uint32_t w = lane; w < kBmWords; w += 32) cnt += __popc(bm[w]);
 #pragma unroll
-            for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
-            // Once the staging area cannot hold them, only count: the warp re-reads its out[] range
-            // after the grid prefix anyway (dense outputs, e.g. cfg5).
-            const bool stage = cnt != 0 && wcount + cnt <= p.c.stg;
-            if (!stage) wcount += cnt;
+                for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
+            }
+            if (!cnt) {  // after a spill, list-only mode still needs this slice's (empty) bitmap
+                if (LIST && wstaged != wcount)
+                    for (uint32_t w = lane; w < kBmWords; w += 32) p.c.bitmap[sl * kBmWords + w] = 0u;
+            } else if (wstaged == wcount && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
 #pragma unroll 1
-            for (uint32_t w0 = 0; stage && w0 < kBmWords; w0 += 32) {
-                uint32_t w = bm[w0 + lane];
-                const uint32_t c = __popc(w);
-                uint32_t incl = c;
+                for (uint32_t w0 = 0; w0 < kBmWords; w0 += 32) {
+                    uint32_t w = bm[w0 + lane];
+                    const uint32_t c = __popc(w);
+                    uint32_t incl = c;
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(~0u, incl, d);
-                    if (lane >= (uint32_t)d) incl += y;
-                }
-                uint64_t r = wcount + incl - c;
-                while (w) {
-                    const uint32_t bit = __ffs(w) - 1;
-                    w &= w - 1;
-                    const uint32_t l = (w0 + lane) * 32 + bit;
-                    if (r < p.c.stg) {
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(~0u, incl, d);
+                        if (lane >= (uint32_t)d) incl += y;
+                    }
+                    uint64_t r = wcount + incl - c;
+                    while (w) {
+                        const uint32_t bit = __ffs(w) - 1;
+                        w &= w - 1;
+                        const uint32_t l = (w0 + lane) * 32 + bit;
                         spos[r] = p.c.pos_base + base + l;
                         spid[r] = ld_cg_u32(out + l);  // written by this warp before the __syncwarp above
+                        ++r;
                     }
-                    ++r;
+                    wcount += __shfl_sync(~0u, incl, 31);
                 }
-                wcount += __shfl_sync(~0u, incl, 31);
+                wstaged = (uint32_t)wcount;
+            } else {  // the staging area is full: spill the slice's bitmap, emit it after the prefix
+                if (wstaged == wcount) spill_rel = (uint32_t)(sl - s_first);
+                if (LIST)  // out[] is valid only at matches: keep the slice's bitmap
+                    for (uint32_t w = lane; w < kBmWords; w += 32) p.c.bitmap[sl * kBmWords + w] = bm[w];
+                wcount += cnt;
             }
         }
     }
     if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
         const uint64_t prefix = grid_prefix<kMWarps>(wcount, p.c.counts, p.c.d_count, s_wcount, s_woff);
-        if (wcount <= p.c.stg) {
-            for (uint64_t i = lane; i < wcount; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);
-        } else {  // staging overflowed (dense matches): re-read this warp's own cells of out[]
-            const uint64_t lo = s_first * kSlice < p.n_own ? s_first * kSlice : p.n_own;
+        for (uint64_t i = lane; i < wstaged; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);
+        // spilled slices (dense matches): stream this warp's out[] from the first spilled slice
+        // (list-only: masked by the spilled slice bitmaps, the scratch holds values only at matches)
+        if (wcount > wstaged) {
+            const uint64_t spill_first = s_first + spill_rel;
+            const uint64_t lo = spill_first * kSlice < p.n_own ? spill_first * kSlice : p.n_own;
             const uint64_t hi = s_end * kSlice < p.n_own ? s_end * kSlice : p.n_own;
-            warp_stream(p.c, lo, hi, prefix,
-                        [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); });
+            warp_stream(
+                p.c, lo, hi, prefix + wstaged,
+                [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); },
+                LIST ? p.c.bitmap : nullptr);
         }
     }
 }
@@ -650,8 +669,22 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
 }
 
 template <bool FUSE>
-static const void *kernel_for(const DeviceImage &img, bool bar) {
+static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false) {
     const MatchPlan &pl = img.plan;
+    if constexpr (FUSE) {
+        if (list) {  // list-only (filter path only; checked by the launcher)
+            if (bar) {
+                if (pl.cell == 2) return pl.all_smem_bar ? (const void *)match_kernel<uint16_t, false, kJumpK16, true, true, true, true>
+                                                         : (const void *)match_kernel<uint16_t, true, kJumpK16, true, true, true, true>;
+                return pl.all_smem_bar ? (const void *)match_kernel<uint32_t, false, kJumpK32, true, true, true, true>
+                                       : (const void *)match_kernel<uint32_t, true, kJumpK32, true, true, true, true>;
+            }
+            if (pl.cell == 2) return pl.all_smem ? (const void *)match_kernel<uint16_t, false, kJumpK16, true, true, false, true>
+                                                 : (const void *)match_kernel<uint16_t, true, kJumpK16, true, true, false, true>;
+            return pl.all_smem ? (const void *)match_kernel<uint32_t, false, kJumpK32, true, true, false, true>
+                               : (const void *)match_kernel<uint32_t, true, kJumpK32, true, true, false, true>;
+        }
+    }
     if (bar) {  // barrier semantics (non-ACGT bytes present): filter path only
         if (pl.cell == 2) return pl.all_smem_bar ? (const void *)match_kernel<uint16_t, false, kJumpK16, FUSE, true, true>
                                                  : (const void *)match_kernel<uint16_t, true, kJumpK16, FUSE, true, true>;
@@ -723,12 +756,12 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_
 int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
-                         void *stream) {
+                         void *stream, bool list_only) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_own == 0) return cudaMemsetAsync(d_count, 0, 8, st);
     MatchArgs a;
     fill_args(a, img, d_packed, n_own, n_avail, d_out);
-    if (d_inv && !img.K2) return cudaErrorNotSupported;
+    if ((d_inv || list_only) && !img.K2) return cudaErrorNotSupported;  // filter path only
     a.inv = d_inv;
     const MatchPlan &pl = img.plan;
     const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
@@ -749,10 +782,12 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.stg = entries / warps;
     c.stage_pos = c.counts + kGMax;
     c.stage_pid = reinterpret_cast<uint32_t *>(c.stage_pos + entries);
+    c.bitmap = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_workspace) + kGMax * 8 +
+                                            ((entries * 12 + 15) & ~15ull));
     c.chunk = a.slices_per_warp * kSlice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    return launch(img, kernel_for<true>(img, d_inv != nullptr), grid, a, true, st);
+    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only), grid, a, true, st);
 }
 
 }  // namespace pfac

@@ -46,29 +46,41 @@ __device__ __forceinline__ bool valid_byte(uint8_t b) {
 // 128-byte store per q).  Grid-stride over the padded word range.
 // inv (nullable): one bit per base, set for a byte outside ACGTacgt (the barriers of reading R5),
 // as one uint16 per packed word; words past the text are written as 0 (their bytes count as valid).
-// first_bad: the warp keeps the first bad index it meets (its iterations ascend) and issues one
-// atomicMin at the end, so a text full of barriers (FASTA newlines) costs one atomic per warp.
-__global__ void __launch_bounds__(256) pack_kernel(const uint8_t *__restrict__ text, uint64_t n,
+// first_bad: a warp reports only the first bad index it meets (its iterations ascend), one atomicMin,
+// so a text full of barriers (FASTA newlines) costs one atomic per warp.
+#ifndef PFAC_PACK_MINB
+#define PFAC_PACK_MINB 8  // 8 CTAs of 256 threads per SM: caps the kernel at 32 registers
+#endif
+template <bool INV>
+__global__ void __launch_bounds__(256, PFAC_PACK_MINB) pack_kernel(const uint8_t *__restrict__ text, uint64_t n,
                                                    uint32_t *__restrict__ packed, uint64_t nwords,
-                                                   uint64_t *first_bad, bool aligned, uint16_t *__restrict__ inv,
-                                                   uint64_t inv_words) {
+                                                   uint64_t *first_bad, bool aligned, uint16_t *__restrict__ inv) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    uint64_t wfirst = ~0ull;  // warp-uniform
+    bool wdone = false;  // warp-uniform: this warp has reported its first bad byte
     for (uint64_t wb = warp * 128; wb < nwords; wb += nwarps * 128) {
-        uint32_t im[4] = {0u, 0u, 0u, 0u};
+        uint32_t bad = 0;  // nonzero: one of this lane's 4 words holds a byte outside ACGTacgt
+        uint32_t mlo = 0, mhi = 0;  // INV: the 4 words' 16-bit masks (q = 0, 1 in mlo; 2, 3 in mhi)
         if (aligned && (wb + 128) * 16 <= n) {
             uint4 v[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) v[q] = ld_stream_v4(text + (wb + 32 * q + lane) * 16);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                uint32_t bq = 0;
-                packed[wb + 32 * q + lane] = pack4(v[q].x, bq) | (pack4(v[q].y, bq) << 8) |
-                                             (pack4(v[q].z, bq) << 16) | (pack4(v[q].w, bq) << 24);
-                if (bq) im[q] = bad16(v[q]);
-                if (inv) inv[wb + 32 * q + lane] = (uint16_t)im[q];
+                if constexpr (INV) {
+                    uint32_t bq = 0;
+                    packed[wb + 32 * q + lane] = pack4(v[q].x, bq) | (pack4(v[q].y, bq) << 8) |
+                                                 (pack4(v[q].z, bq) << 16) | (pack4(v[q].w, bq) << 24);
+                    const uint32_t m = bq ? bad16(v[q]) : 0u;
+                    inv[wb + 32 * q + lane] = (uint16_t)m;
+                    if (q < 2) mlo |= m << (16 * q);
+                    else mhi |= m << (16 * (q - 2));
+                    bad |= bq;
+                } else {  // one accumulator: the integer pipe is this kernel's limit
+                    packed[wb + 32 * q + lane] = pack4(v[q].x, bad) | (pack4(v[q].y, bad) << 8) |
+                                                 (pack4(v[q].z, bad) << 16) | (pack4(v[q].w, bad) << 24);
+                }
             }
         } else {
 #pragma unroll 1
@@ -85,23 +97,38 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t *__restrict__ t
                         word |= (t ^ (t >> 1)) << (2 * j);
                     }
                 }
-                im[q] = m;
+                bad |= m;
                 packed[w] = word;
-                if (inv) inv[w] = (uint16_t)m;
+                if (INV) {
+                    inv[w] = (uint16_t)m;
+                    if (q < 2) mlo |= m << (16 * q);
+                    else mhi |= m << (16 * (q - 2));
+                }
             }
         }
-        if (first_bad && wfirst == ~0ull) {
-            // this lane's first bad byte: its first word with one (offsets of later q are larger)
+        if (first_bad && !wdone && __any_sync(~0u, bad != 0)) {
+            // rare (once per warp): this lane's first bad byte (its words ascend with q)
             uint32_t off = ~0u;
-#pragma unroll
-            for (int q = 3; q >= 0; --q)
-                if (im[q]) off = (32u * q + lane) * 16u + (__ffs(im[q]) - 1);
+            if constexpr (INV) {  // from the masks in registers
+                for (uint32_t q = 0; q < 4 && off == ~0u; ++q) {
+                    const uint32_t m = ((q < 2 ? mlo : mhi) >> (16 * (q & 1))) & 0xFFFFu;
+                    if (m) off = (32u * q + lane) * 16u + (__ffs(m) - 1);
+                }
+            } else {  // rescan this lane's bytes (pfac_pack_async on a text with barriers)
+                for (uint32_t q = 0; bad && q < 4 && off == ~0u; ++q) {
+                    const uint64_t w = wb + 32 * q + lane;
+                    for (uint32_t j = 0; j < 16; ++j)
+                        if (w * 16 + j < n && !valid_byte(text[w * 16 + j])) {
+                            off = (32u * q + lane) * 16u + j;
+                            break;
+                        }
+                }
+            }
             off = __reduce_min_sync(~0u, off);
-            if (off != ~0u) wfirst = wb * 16 + off;
+            if (lane == 0) atomicMin(reinterpret_cast<unsigned long long *>(first_bad), (unsigned long long)(wb * 16 + off));
+            wdone = true;  // later iterations of this warp only see larger positions
         }
     }
-    if (first_bad && lane == 0 && wfirst != ~0ull)
-        atomicMin(reinterpret_cast<unsigned long long *>(first_bad), (unsigned long long)wfirst);
 }
 
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,
@@ -124,8 +151,12 @@ int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t 
     const uint64_t cap = (uint64_t)sms * 8;
     if (blocks > cap) blocks = cap;
     const bool aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
-    pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_text, n, d_packed, nwords_padded, d_first_bad, aligned, d_inv,
-                                                   inv_words);
+    if (d_inv)
+        pack_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(d_text, n, d_packed, nwords_padded, d_first_bad, aligned,
+                                                            d_inv);
+    else
+        pack_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(d_text, n, d_packed, nwords_padded, d_first_bad, aligned,
+                                                             nullptr);
     return cudaGetLastError();
 }
 

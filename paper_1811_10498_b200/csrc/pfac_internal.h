@@ -140,7 +140,7 @@ uint64_t compact_workspace_bytes(uint64_t n);
 int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
-                         void *stream);
+                         void *stream, bool list_only = false);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
                   const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,

@@ -269,7 +269,16 @@ def _full_config(idx):
     assert (pos2[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
     assert (pid2[:len(epos)].cpu().numpy() == epid).all()
     assert bool((out2 == out).all())
-    del out2, packed
+    del out2
+    # the list-only path (no dense out[]) on the same full input
+    ws = torch.empty(P.match_list_workspace_bytes(n), dtype=torch.uint8, device=DEV)
+    pos2.fill_(-1)
+    P.match_list_async(a, packed, n, n, pos2, pid2, cnt, ws)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == len(epos)
+    assert (pos2[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
+    assert (pid2[:len(epos)].cpu().numpy() == epid).all()
+    del packed, ws
     # sampled out[] windows (every element, including the zeros)
     o = Oracle(pats)
     n = len(text)
