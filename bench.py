@@ -48,7 +48,9 @@ def profiled_traffic(cfg_idx: int, path: str):
         return None
     with open(p) as f:
         d = json.load(f)
-    e = d.get(f"cfg{cfg_idx}", {}).get("match_fused" if path == "fused" else "match")
+    key = {"fused": "match_fused", "separate": "match", "list": "match_list", "text": "match_text",
+           "text-list": "match_text_list"}[path]
+    e = d.get(f"cfg{cfg_idx}", {}).get(key)
     return None if e is None else float(e["dram_bytes_per_launch"])
 
 
@@ -248,12 +250,18 @@ def run_pfac(args):
     pos = torch.empty(cap, dtype=torch.int64, device=dev)
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    fused = args.path in ("fused", "list")
-    list_only = args.path == "list"
-    if list_only:  # the list without the dense out[] (scratch workspace)
+    fused = args.path in ("fused", "list", "text", "text-list")
+    list_only = args.path in ("list", "text-list")
+    text_in = args.path in ("text", "text-list")  # pack fused into the match kernel (pfac_match_text_async)
+    if text_in:
+        ws = torch.empty(P.match_text_workspace_bytes(n_own, n_avail, list_only), dtype=torch.uint8, device=dev)
+    elif list_only:  # the list without the dense out[] (scratch workspace)
         ws = torch.empty(P.match_list_workspace_bytes(n_own), dtype=torch.uint8, device=dev)
     graph_error = None
-    kernels_per_step = (2 if fused else 3) + (1 if args.all_matches else 0)
+    # text path: one kernel when the image's plan takes it (pfac_image_info.text_kernel), else pack +
+    # first-bad scan + fused kernel inside the call
+    text_one = text_in and a.image_info(local)["text_kernel"] == 1 and d_text.data_ptr() % 16 == 0
+    kernels_per_step = (1 if text_one else 3 if text_in else 2 if fused else 3) + (1 if args.all_matches else 0)
     if args.all_matches:  # every occurrence: size the output from a probe
         ws_e = torch.empty(P.expand_workspace_bytes(), dtype=torch.uint8, device=dev)
         count_all = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -267,10 +275,17 @@ def run_pfac(args):
         st = stream if st is None else st
         if ev is not None:
             ev[0].record(st)
-        pack(st)
+        if not text_in:
+            pack(st)
         if ev is not None:
             ev[1].record(st)
-        if list_only:
+        if text_in:  # one kernel from the ASCII text: pack + match + compact
+            P.match_text_async(a, d_text, n_own, n_avail, None if list_only else out, pos, pid, count, ws,
+                               pos_base=sh.start, first_bad=bad, stream=st)
+            if ev is not None:
+                ev[2].record(st)
+                ev[3].record(st)
+        elif list_only:
             P.match_list_async(a, packed, n_own, n_avail, pos, pid, count, ws, pos_base=sh.start, inv=inv,
                                stream=st)
             if ev is not None:
@@ -371,6 +386,11 @@ def run_pfac(args):
     match_bpb = MATCH_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
     if list_only:  # packed text read + 12 B per match written (no out[])
         match_bpb = 0.25 + (BARRIER_BYTES_PER_BASE if bars else 0.0) + 12.0 * m_final / max(1, n_own)
+    if text_one:  # ASCII text read (1 B/base) + out[] written (4 B/base; list only: 12 B per match)
+        match_bpb = 1.0 + (12.0 * m_final / max(1, n_own) if list_only else 4.0)
+    elif text_in:  # the call's pack + first-bad + fused kernels: their bytes together
+        match_bpb = (PACK_BYTES_PER_BASE + 2 * BARRIER_BYTES_PER_BASE + 0.25 +
+                     (12.0 * m_final / max(1, n_own) if list_only else 4.0))
     pack_bpb = PACK_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
     match_gbs = match_bpb * n_own / (match_ms * 1e-3) / 1e9
     traffic = profiled_traffic(args.config, args.path) if args.n is None and not bars else None
@@ -430,16 +450,19 @@ def run_pfac(args):
                        "matches_per_step": m_final, "image": a.image_info(local)},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
-                         "kernel": ("match_kernel<FUSE=1, list-only>" if list_only else
+                         "kernel": ("match_kernel<TXT=1> (pack + match + compact)" if text_one and not list_only else
+                                    "match_kernel<TXT=1, list-only> (pack + match + list)" if text_one else
+                                    "pack + match_kernel<FUSE=1,BAR=1> (two-kernel text path)" if text_in else
+                                    "match_kernel<FUSE=1, list-only>" if list_only else
                                     "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel")
                          + ("<BAR=1>" if bars else ""),
                          "algorithmic_bytes_per_launch": match_bpb * n_own, "peak_source": hbm_src},
-            "path": args.path,
+            "path": args.path + (" (one kernel)" if text_one else " (pack + fused kernel)" if text_in else ""),
             "cuda_graph": graph is not None, **({"cuda_graph_error": graph_error} if graph_error else {}),
             "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,
                            "compact": None if fused else compact_ms,
                            **({"expand": expand_ms, "occurrences": int(count_all.item())} if args.all_matches else {}),
-                           "pack_frac": pack_bpb * n_own / (pack_ms * 1e-3) / 1e9 / hbm,
+                           "pack_frac": (pack_bpb * n_own / (pack_ms * 1e-3) / 1e9 / hbm if not text_in else None),
                            "compact_frac": (COMPACT_BYTES_PER_BASE * n_own / (compact_ms * 1e-3) / 1e9 / hbm
                                             if compact_ms > 0 else None)},
             "match_gbases_per_s_per_gpu": n_own / (match_ms * 1e-3) / 1e9,
@@ -466,9 +489,11 @@ def main():
                     help="launch the step's kernels directly instead of replaying one captured CUDA graph")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="process group for N>1 (gloo only to test the multi-rank flow on one GPU)")
-    ap.add_argument("--path", choices=["fused", "separate", "list"], default="fused",
-                    help="fused: pack -> match+compact kernel; separate: pack -> match -> compact; "
-                         "list: pack -> list-only match (no dense out[])")
+    ap.add_argument("--path", choices=["fused", "separate", "list", "text", "text-list"], default="text",
+                    help="text (default): pfac_match_text_async, one kernel from the ASCII text where the "
+                         "image's plan prefers it (else pack -> match+compact inside the call); fused: pack -> match+compact kernel; separate: pack -> match -> compact; "
+                         "list: pack -> list-only match (no dense out[]); text: one kernel from the ASCII "
+                         "text (pack + match + compact); text-list: the same without out[]")
     ap.add_argument("--bases-per-rank", dest="n", type=int, default=None, help="override bases per rank (testing)")
     ap.add_argument("--barriers", type=int, default=None, metavar="LINE",
                     help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")

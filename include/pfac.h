@@ -178,6 +178,31 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
                           void *d_workspace, void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Match from the ASCII text in one kernel (pack fused into the match + compact kernel): the same
+ * results as pfac_pack_barriers_async -> pfac_match_compact_barriers_async (or, d_out == NULL, ->
+ * pfac_match_list_async) on d_text[0..n_avail), positions [0, n_own), without the packed and
+ * barrier-mask arrays in HBM.  Definition: out[i] = id of the longest pattern starting at i
+ * (PAPER.md:91, :204-207); bytes outside ACGTacgt are barriers (reading R5).
+ *   d_text     device, n_avail bytes (16-byte aligned for the one-kernel path; otherwise, or when
+ *              the automaton's halo is too long for its shared-memory plan (max_len > ~112), the
+ *              call runs the two-kernel GPU path through buffers in d_workspace -- same results)
+ *   d_out      device int32[n_own], 16-byte aligned, or NULL: list only (no dense out[])
+ *   d_pos/d_pid/capacity/d_count/d_hist/pos_base: as pfac_match_compact_async
+ *   d_first_bad (nullable, device uint64): pos_base + the first owned index (< n_own) whose byte
+ *              is not ACGTacgt, or UINT64_MAX
+ *   d_workspace: pfac_match_text_workspace_bytes(n_own, n_avail, d_out == NULL) bytes, 16-byte
+ *              aligned, any content.
+ * Errors: PFAC_E_ARG (null / misaligned / n_avail < n_own), PFAC_E_CUDA (launch; images built
+ * without the filter, PFAC_FB16=0).  Asynchronous (a cooperative launch); a list longer than
+ * capacity is reported through *d_count > capacity (read it after a sync).
+ */
+uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int list_only);
+int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64_t n_own, uint64_t n_avail,
+                          int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                          uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad,
+                          void *d_workspace, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * End to end over HOST memory (the call a user with a text in RAM makes): the match list
  * {(pos_base + i, out[i]) : out[i] != 0, i < n_own} of the ASCII text h_text[0..n_avail) (walks
  * read up to n_avail >= n_own: a shard and its halo) on CUDA device `device`.  The text is streamed
@@ -233,6 +258,8 @@ typedef struct {
     uint64_t smem_bytes;      /* dynamic shared memory per CTA of the match kernel */
     uint64_t l2_persist_bytes;/* access-policy window over J2 */
     uint64_t image_bytes;     /* device memory of the image */
+    uint32_t text_kernel;     /* 1: pfac_match_text_async runs the one-kernel path on aligned text */
+    uint32_t text_window_rows;/* rows staged in shared memory by that kernel */
 } pfac_image_info_t;
 int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out);
 

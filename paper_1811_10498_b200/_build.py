@@ -10,7 +10,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libpfac.so")
 SOURCES = ["api.cu", "match.cu", "pack.cu", "compact.cu", "expand.cu", "builder.cpp"]
-HEADERS = ["pfac_internal.h", "ptx.cuh", os.path.join("..", "..", "include", "pfac.h")]
+HEADERS = ["pfac_internal.h", "ptx.cuh", "pack_common.cuh", "compact_common.cuh", os.path.join("..", "..", "include", "pfac.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -55,6 +55,11 @@ _SIGS = {
                                                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                                          ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_match_text_workspace_bytes": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]),
+    "pfac_match_text_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_prefix_chain": (ctypes.c_void_p, [ctypes.c_void_p]),
     "pfac_expand_workspace_bytes": (ctypes.c_uint64, []),
     "pfac_expand_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -101,7 +106,8 @@ class ImageInfo(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("cell_bytes", ctypes.c_uint32), ("K", ctypes.c_uint32),
                 ("K2", ctypes.c_uint32), ("states", ctypes.c_uint32), ("window_rows", ctypes.c_uint32),
                 ("all_smem", ctypes.c_uint32), ("short_pat", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint64),
-                ("l2_persist_bytes", ctypes.c_uint64), ("image_bytes", ctypes.c_uint64)]
+                ("l2_persist_bytes", ctypes.c_uint64), ("image_bytes", ctypes.c_uint64),
+                ("text_kernel", ctypes.c_uint32), ("text_window_rows", ctypes.c_uint32)]
 
 
 class PfacError(RuntimeError):
@@ -372,3 +378,17 @@ def match_list_async(a: Automaton, packed, n_own: int, n_avail: int, pos, pid, c
     _check(lib().pfac_match_list_async(a.handle, _ptr(packed), _ptr(inv), n_own, n_avail, pos_base, _ptr(pos),
                                        _ptr(pid), pos.numel(), _ptr(count), _ptr(hist), _ptr(workspace),
                                        _stream(stream, count.device)))
+
+
+def match_text_workspace_bytes(n_own: int, n_avail: int | None = None, list_only: bool = False) -> int:
+    return int(lib().pfac_match_text_workspace_bytes(n_own, n_own if n_avail is None else n_avail, int(list_only)))
+
+
+def match_text_async(a: Automaton, text, n_own: int, n_avail: int, out, pos, pid, count, workspace,
+                     pos_base: int = 0, hist=None, first_bad=None, stream=None):
+    """pfac_match_text_async: pack + match + ordered match list from the ASCII text in one kernel.
+    out=None: list only.  count / first_bad: 1-element int64 CUDA tensors; workspace:
+    match_text_workspace_bytes(n_own, n_avail, out is None) bytes."""
+    _check(lib().pfac_match_text_async(a.handle, _ptr(text), n_own, n_avail, _ptr(out), pos_base, _ptr(pos),
+                                       _ptr(pid), pos.numel(), _ptr(count), _ptr(hist), _ptr(first_bad),
+                                       _ptr(workspace), _stream(stream, count.device)))

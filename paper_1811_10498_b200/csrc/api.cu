@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -314,6 +315,67 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
     int e = launch_match_compact(*im, a->k, d_packed, d_inv, n_own, n_avail, scratch, pos_base, d_pos, d_pid, capacity,
                                  d_count, d_hist, d_workspace, stream, true);
     return e ? cuda_fail(e, "pfac_match_list_async") : PFAC_OK;
+}
+
+static uint64_t al16(uint64_t x) { return (x + 15) & ~15ull; }
+
+// Whether pfac_match_text_async runs the one-kernel path for this image: the plan's measured
+// preference (MatchPlan::txt_pref), overridden by PFAC_TEXT_KERNEL=0 (never) / 1 (whenever it fits).
+static bool text_kernel_for(const DeviceImage &im) {
+    const char *e = getenv("PFAC_TEXT_KERNEL");  // read per call (tests switch it)
+    const int env = e && *e ? atoi(e) : -1;
+    if (!im.K2 || !im.plan.txt_ok || env == 0) return false;
+    return env == 1 || im.plan.txt_pref;
+}
+
+uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int list_only) {
+    // [compaction workspace | list-only out[] scratch | two-kernel path: packed words | barrier words]
+    return al16(compact_workspace_bytes(n_own)) + (list_only ? al16(n_own * 4) : 0) +
+           al16(pfac_packed_words(n_avail) * 4) + al16(pfac_inv_words(n_avail) * 2) + 16;
+}
+
+int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64_t n_own, uint64_t n_avail,
+                          int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                          uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad, void *d_workspace,
+                          void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match_text_async: null automaton");
+    if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_text_async: n_avail < n_own");
+    if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_match_text_async: null d_count / d_workspace");
+    if (capacity > 0 && (!d_pos || !d_pid)) return fail(PFAC_E_ARG, "pfac_match_text_async: null d_pos / d_pid");
+    if (n_own > 0 && !d_text) return fail(PFAC_E_ARG, "pfac_match_text_async: null d_text");
+    if (!aligned16(d_workspace) || (d_out && !aligned16(d_out)))
+        return fail(PFAC_E_ARG, "pfac_match_text_async: d_out and d_workspace must be 16-byte aligned");
+    const int dev = device_of(d_count);
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match_text_async: d_count is not device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_own == 0) {
+        cudaError_t e = cudaMemsetAsync(d_count, 0, 8, st);
+        if (e == cudaSuccess && d_first_bad) e = cudaMemsetAsync(d_first_bad, 0xFF, 8, st);
+        return e ? cuda_fail(e, "pfac_match_text_async") : PFAC_OK;
+    }
+    DeviceImage *im = nullptr;
+    int rc = get_image(a, dev, &im);
+    if (rc) return rc;
+    uint8_t *ws = reinterpret_cast<uint8_t *>(d_workspace);
+    const bool list_only = d_out == nullptr;
+    uint8_t *after = ws + al16(compact_workspace_bytes(n_own));
+    int32_t *out = list_only ? reinterpret_cast<int32_t *>(after) : d_out;
+    if (list_only) after += al16(n_own * 4);
+    int e;
+    if (text_kernel_for(*im) && aligned16(d_text)) {
+        e = launch_match_compact(*im, a->k, nullptr, nullptr, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
+                                 d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad);
+    } else {  // two kernels through the workspace (unaligned text, or a halo too long for the plan)
+        uint32_t *packed = reinterpret_cast<uint32_t *>(after);
+        uint16_t *inv = reinterpret_cast<uint16_t *>(after + al16(pfac_packed_words(n_avail) * 4));
+        // first_bad over the owned range [0, n_own) only, from the barrier bits
+        e = launch_pack(d_text, n_avail, packed, pfac_packed_words(n_avail), nullptr, inv, stream);
+        if (!e && d_first_bad) e = launch_first_bad_inv(inv, n_own, pos_base, d_first_bad, stream);
+        if (!e)
+            e = launch_match_compact(*im, a->k, packed, inv, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
+                                     d_count, d_hist, d_workspace, stream, list_only);
+    }
+    return e ? cuda_fail(e, "pfac_match_text_async") : PFAC_OK;
 }
 
 int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
@@ -640,6 +702,8 @@ int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out)
     out->smem_bytes = im->plan.smem;
     out->l2_persist_bytes = im->l2_persist_bytes;
     out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4 + h.FB.size() * 4;
+    out->text_kernel = text_kernel_for(*im) ? 1u : 0u;
+    out->text_window_rows = im->plan.window_txt;
     return PFAC_OK;
 }
 

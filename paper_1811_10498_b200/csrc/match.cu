@@ -21,12 +21,19 @@
 //  * FUSE (pfac_match_compact_async): nonzero results also set bits in a per-slice match bitmap; at
 //    the end of each slice the warp stages its matches in position order, and a grid-wide count
 //    prefix (cooperative launch) places every warp's list.
+//  * TXT (pfac_match_text_async): the same fused kernel reading the ASCII text itself -- the pack step
+//     moves into the kernel.  Each warp's lane 0 fetches the slice's ASCII
+//    bytes (+ halo) by TMA into a shared staging buffer; the warp packs them into its 2-bit slice
+//    buffer and the barrier bits (reading R5) in shared memory, then lane 0 prefetches the next
+//    slice's bytes while the warp matches this one.  Slices with a non-ACGT byte take the barrier
+//    path.  HBM traffic per base: 1 B of ASCII read + 4 B of out[] written (vs 1.25 + 4.25 split).
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <type_traits>
 
 #include "compact_common.cuh"
+#include "pack_common.cuh"
 #include "pfac_internal.h"
 #include "ptx.cuh"
 
@@ -77,6 +84,8 @@ struct MatchArgs {
     uint32_t bar_dead;     // BAR: (1 << min(minlen, K1)) - 1: a barrier this close ends every match
     uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
     CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
+    const uint8_t *text;   // TXT: the ASCII text (n_avail bytes, 16-byte aligned)
+    uint64_t *first_bad;   // TXT (nullable): atomicMin of pos_base + the first owned non-ACGT index
 };
 
 // One T row (4 cells).  Branch row: child per base.  Chain row: flag|L, then L forced bases.
@@ -181,15 +190,20 @@ constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared me
 static __host__ __device__ constexpr uint32_t inv_buf_words(uint32_t slice_words) {  // uint16, 16-B multiple
     return (slice_words + 8 + 7) & ~7u;
 }
-static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, bool bar = false) {
-    return 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4 +  // text, mbarriers, queue, bitmap
-           (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);                // BAR: the slice's barrier bits
+static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, bool bar = false, bool txt = false) {
+    // TXT: ASCII staging (slice_words * 16 bytes) + ONE packed slice and barrier-bit buffer (the warp
+    // packs a slice before it prefetches the next one's bytes, so the ASCII buffer is the double buffer)
+    return txt ? slice_words * 16 + (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4 +
+                     inv_buf_words(slice_words) * 2
+               : 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4 +  // text, mbarriers, queue, bitmap
+                     (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);          // BAR: the slice's barrier bits
 }
 
-template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false>
+template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false, bool TXT = false>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
+    static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
@@ -201,17 +215,18 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     CT *sT = reinterpret_cast<CT *>(smem + (FBM ? kFBBytes : NJ * sizeof(CT)));
     CT *sF = sT + (size_t)p.window * 4;
     uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + p.window);  // 16-byte aligned (W % 8 == 0)
-    const uint32_t WB = warp_bytes(p.slice_words, BAR);
+    const uint32_t WB = warp_bytes(p.slice_words, BAR, TXT);
     uint64_t *tab_bar = reinterpret_cast<uint64_t *>(wbase + kMWarps * WB);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t *txt0 = reinterpret_cast<uint32_t *>(wbase + warp * WB);
-    uint32_t *txt1 = txt0 + p.slice_words + 4;
+    uint8_t *asc = wbase + warp * WB;  // TXT: the slice's ASCII bytes (TMA destination)
+    uint32_t *txt0 = reinterpret_cast<uint32_t *>(asc + (TXT ? p.slice_words * 16 : 0));
+    uint32_t *txt1 = TXT ? txt0 : txt0 + p.slice_words + 4;
     uint64_t *bar = reinterpret_cast<uint64_t *>(txt1 + p.slice_words + 4);
     uint16_t *queue = reinterpret_cast<uint16_t *>(bar + 2);
     uint32_t *bm = reinterpret_cast<uint32_t *>(queue + kQCap);  // fused: nonzero cells of the slice
     uint16_t *inv0 = reinterpret_cast<uint16_t *>(bm + kBmWords);  // BAR: barrier bits of the slice
-    uint16_t *inv1 = inv0 + inv_buf_words(p.slice_words);
+    uint16_t *inv1 = TXT ? inv0 : inv0 + inv_buf_words(p.slice_words);
     const uint32_t lt = (1u << lane) - 1;
     __shared__ uint64_t s_wcount[kMWarps], s_woff[kMWarps];
 
@@ -227,6 +242,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     constexpr bool DIRECT = PFAC_TEXT_DIRECT && !BAR;
     auto issue = [&](uint64_t sl, uint32_t *dst, uint64_t *b) {
         if constexpr (DIRECT) return;
+        if constexpr (TXT) {  // the 16-byte multiple part of the slice's readable bytes (the rest: lanes)
+            const uint64_t b0 = sl * kSlice, left = p.n_avail - b0;
+            const uint32_t nb = (uint32_t)(left < p.slice_words * 16ull ? left : p.slice_words * 16ull) & ~15u;
+            mbar_expect_tx(b, nb);
+            if (nb) bulk_g2s(asc, p.text + b0, nb, b);
+            return;
+        }
         const uint64_t w0 = sl * (kSlice / 16);
         const uint64_t left = p.avail_words - w0;
         const uint32_t nw = left < p.slice_words ? (uint32_t)left : p.slice_words;
@@ -266,16 +288,18 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint64_t wcount = 0;   // fused: matches of this warp so far
     uint32_t wstaged = 0;     // fused: of which staged (<= stg; the rest are streamed after the prefix)
     uint32_t spill_rel = ~0u; // fused: first spilled slice, relative to s_first
+    bool bad_done = false;    // TXT: this warp has reported its first non-ACGT byte (slices ascend)
     uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
     uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
     for (uint64_t sl = s_first; sl < s_end; sl += s_stride, ++it) {
         const uint32_t buf = it & 1;
-        if (lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
+        if (!TXT && lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
             if (FUSE) {
             for (uint32_t w = lane; w < kBmWords; w += 32) bm[w] = 0;
             __syncwarp();
         }
-        if constexpr (!DIRECT) mbar_wait(&bar[buf], (it >> 1) & 1);
+        if constexpr (TXT) mbar_wait(&bar[0], it & 1);
+        else if constexpr (!DIRECT) mbar_wait(&bar[buf], (it >> 1) & 1);
         const uint32_t *txt = DIRECT ? p.packed + sl * (kSlice / 16) : (buf ? txt1 : txt0);
         const uint16_t *inv = buf ? inv1 : inv0;
         (void)inv;
@@ -287,7 +311,55 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         int32_t *out = p.out + base;
         // BAR: does any readable base of this slice (owned range + halo) fail to be ACGT?
         bool bar_slice = false;
-        if constexpr (BAR) {
+        if constexpr (TXT) {
+            // Pack the slice (16 bases per lane and step, PAPER.md:120's 4-letter alphabet as 2-bit
+            // codes); bytes past the readable end pack as A.  The hot pass only learns whether a byte
+            // outside ACGTacgt exists; the rare exact pass writes the barrier bits (reading R5).
+            const uint32_t nb = lend & ~15u;  // bytes the TMA brought; [nb, lend) come from global
+            uint32_t acc = 0;
+            for (uint32_t q = lane; q < p.slice_words + 4; q += 32) {
+                uint32_t word = 0;
+                if (q * 16 + 16 <= nb) {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(asc + q * 16);
+                    word = pack16(v.x, v.y, v.z, v.w, acc);
+                } else if (q * 16 < lend) {
+                    for (uint32_t j = 0; j < 16 && q * 16 + j < lend; ++j) {
+                        const uint32_t i = q * 16 + j;
+                        const uint8_t b = i < nb ? asc[i] : p.text[base + i];
+                        acc |= valid_byte(b) ? 0u : 1u;
+                        word |= (((b >> 1) ^ (b >> 2)) & 3u) << (2 * j);
+                    }
+                }
+                txt0[q] = word;
+            }
+            bar_slice = __any_sync(~0u, (acc & kBadMask) != 0);
+            if (bar_slice) {
+                uint32_t firstb = ~0u;
+                for (uint32_t q = lane; q < inv_buf_words(p.slice_words); q += 32) {
+                    uint32_t m = 0;
+                    if (q * 16 + 16 <= nb) {
+                        m = bad16(*reinterpret_cast<const uint4 *>(asc + q * 16));
+                    } else if (q * 16 < lend) {
+                        for (uint32_t j = 0; j < 16 && q * 16 + j < lend; ++j) {
+                            const uint32_t i = q * 16 + j;
+                            m |= valid_byte(i < nb ? asc[i] : p.text[base + i]) ? 0u : 1u << j;
+                        }
+                    }
+                    inv0[q] = (uint16_t)m;
+                    const uint32_t mo = q * 16 < lown ? (lown - q * 16 >= 16 ? m : m & ((1u << (lown - q * 16)) - 1)) : 0u;
+                    if (mo && firstb == ~0u) firstb = q * 16 + (__ffs(mo) - 1);  // q ascends per lane
+                }
+                firstb = __reduce_min_sync(~0u, firstb);
+                if (p.first_bad && !bad_done && firstb != ~0u) {
+                    if (lane == 0)
+                        atomicMin(reinterpret_cast<unsigned long long *>(p.first_bad),
+                                  (unsigned long long)(p.c.pos_base + base + firstb));
+                    bad_done = true;
+                }
+            }
+            __syncwarp();  // the ASCII buffer is free: fetch the next slice while this one is matched
+            if (lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, txt0, &bar[0]);
+        } else if constexpr (BAR) {
             uint32_t any = 0;
             for (uint32_t w = lane; w < (lend + 15) / 16; w += 32) any |= inv[w];
             bar_slice = __any_sync(~0u, any) != 0;
@@ -600,11 +672,15 @@ static void dev_props(int device, int &sms, int &optin) {
 #define PFAC_WINDOW_MIN_SHARE 4
 #endif
 constexpr uint32_t kWindowMinShare = PFAC_WINDOW_MIN_SHARE;  // keep a row window only if rows <= this x window
-constexpr size_t kStaticSmemReserve = 1024;  // the fused kernel's static shared arrays (grid_prefix)
+constexpr size_t kStaticSmemReserve = 1024;
+#ifndef PFAC_TXT_MAX_ROWS
+#define PFAC_TXT_MAX_ROWS (1u << 20)
+#endif
+constexpr uint32_t kTxtMaxRows = PFAC_TXT_MAX_ROWS;  // larger automata keep the two-kernel text path  // the fused kernel's static shared arrays (grid_prefix)
 
 static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
-                         bool bar = false) {
-    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words, bar) + 16;
+                         bool bar = false, bool txt = false) {
+    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt) + 16;
 }
 
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
@@ -639,6 +715,23 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     pl.all_smem_bar = wb >= h.rows;
     pl.window_bar = pl.all_smem_bar ? h.rows : wb;
     pl.smem_bar = match_smem(table, pl.cell, pl.window_bar, pl.slice_words, true);
+    // text-input variant (TXT): the ASCII staging buffers take the room of the row window; it exists
+    // only when the filter image fits beside them (halo <= 112 bases at 896 threads per CTA)
+    const size_t fixed_t = match_smem(table, pl.cell, 0, pl.slice_words, true, true) + kStaticSmemReserve;
+    pl.txt_ok = h.K2 != 0 && (size_t)optin >= fixed_t;
+    uint32_t wt = pl.txt_ok ? (uint32_t)(((size_t)optin - fixed_t) / (5 * pl.cell)) & ~7u : 0u;
+    if (wt < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wt) wt = 0;
+#ifdef PFAC_WINDOW_MAX
+    if (wt > (uint32_t)(PFAC_WINDOW_MAX)) wt = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
+#endif
+    pl.all_smem_txt = wt >= h.rows;
+    pl.window_txt = pl.all_smem_txt ? h.rows : wt;
+    pl.smem_txt = match_smem(table, pl.cell, pl.window_txt, pl.slice_words, true, true);
+    // Measured (profiles/): the one-kernel text path wins where the step is HBM-bound
+    // (cfg2 +11%, cfg3 +13%); it loses where walks dominate and the two-kernel plan holds every row in
+    // shared memory (cfg5 -5%) or the rows are many and L1 caches them (cfg4, 5.4 M states: -12%;
+    // the text buffers take that L1).
+    pl.txt_pref = pl.txt_ok && !(pl.all_smem && !pl.all_smem_txt) && h.rows <= kTxtMaxRows;
     pl.sms = sms;
     return pl;
 }
@@ -666,12 +759,24 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.slices_per_warp = 0;
     a.inv = nullptr;
     a.c = CompactArgs{};
+    a.text = nullptr;
+    a.first_bad = nullptr;
+}
+
+template <typename CT, bool LIST>
+static const void *txt_kernel(bool all_smem) {
+    return all_smem ? (const void *)match_kernel<CT, false, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true>
+                    : (const void *)match_kernel<CT, true, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true>;
 }
 
 template <bool FUSE>
-static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false) {
+static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false, bool txt = false) {
     const MatchPlan &pl = img.plan;
     if constexpr (FUSE) {
+        if (txt) {  // text input (filter path; checked by the launcher)
+            if (pl.cell == 2) return list ? txt_kernel<uint16_t, true>(pl.all_smem_txt) : txt_kernel<uint16_t, false>(pl.all_smem_txt);
+            return list ? txt_kernel<uint32_t, true>(pl.all_smem_txt) : txt_kernel<uint32_t, false>(pl.all_smem_txt);
+        }
         if (list) {  // list-only (filter path only; checked by the launcher)
             if (bar) {
                 if (pl.cell == 2) return pl.all_smem_bar ? (const void *)match_kernel<uint16_t, false, kJumpK16, true, true, true, true>
@@ -706,8 +811,9 @@ static const void *kernel_for(const DeviceImage &img, bool bar, bool list = fals
 static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchArgs &a, bool cooperative,
                   cudaStream_t st) {
     const MatchPlan &pl = img.plan;
-    const size_t smem = a.inv ? pl.smem_bar : pl.smem;
-    if (a.inv) a.window = pl.window_bar;
+    const size_t smem = a.text ? pl.smem_txt : a.inv ? pl.smem_bar : pl.smem;
+    if (a.text) a.window = pl.window_txt;
+    else if (a.inv) a.window = pl.window_bar;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -756,13 +862,20 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_
 int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
-                         void *stream, bool list_only) {
+                         void *stream, bool list_only, const uint8_t *d_text, uint64_t *d_first_bad) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (d_text && d_first_bad) {
+        cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, 8, st);
+        if (e != cudaSuccess) return e;
+    }
     if (n_own == 0) return cudaMemsetAsync(d_count, 0, 8, st);
     MatchArgs a;
     fill_args(a, img, d_packed, n_own, n_avail, d_out);
-    if ((d_inv || list_only) && !img.K2) return cudaErrorNotSupported;  // filter path only
+    if ((d_inv || list_only || d_text) && !img.K2) return cudaErrorNotSupported;  // filter path only
+    if (d_text && !img.plan.txt_ok) return cudaErrorNotSupported;
     a.inv = d_inv;
+    a.text = d_text;
+    a.first_bad = d_text ? d_first_bad : nullptr;
     const MatchPlan &pl = img.plan;
     const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
     const uint64_t warps = grid * kMWarps;
@@ -787,7 +900,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.chunk = a.slices_per_warp * kSlice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only), grid, a, true, st);
+    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr), grid, a, true, st);
 }
 
 }  // namespace pfac

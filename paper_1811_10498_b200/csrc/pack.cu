@@ -5,42 +5,12 @@
 #include <cstdint>
 
 #include "pfac_internal.h"
+#include "pack_common.cuh"
 #include "ptx.cuh"
 
 namespace pfac {
 
 // ============================================================================ pack
-// ASCII -> 2-bit codes (A0 C1 G2 T3), 16 bases per uint32, base j at bits 2(j mod 16).
-// Four bytes at a time (one 32-bit word x):
-//   t = (x >> 1) & 3 per byte gives A0 C1 T2 G3 for upper and lower case;
-//   validity: the byte must equal "acgt"[t] after |0x20 -- one PRMT builds the expected word;
-//   code = t ^ (t >> 1) swaps G and T; one multiply gathers the four 2-bit codes into a byte.
-// Integer ALU (LOP3/SHF/PRMT) is the scarce pipe here (half rate), so the multiply does the gather.
-__device__ __forceinline__ uint32_t expect4(uint32_t x, uint32_t t) {  // nonzero bytes = bad bytes
-    uint32_t sel = t | (t >> 4);                    // nibble selectors at bits 0, 4, 16, 20
-    sel = (sel & 0xFFu) | ((sel >> 8) & 0xFF00u);   // -> bits 0, 4, 8, 12
-    return __byte_perm(0x67746361u, 0u, sel) ^ (x | 0x20202020u);  // "acgt"[t] vs the byte
-}
-__device__ __forceinline__ uint32_t pack4(uint32_t x, uint32_t &bad) {
-    const uint32_t t = (x >> 1) & 0x03030303u;
-    bad |= expect4(x, t);
-    const uint32_t c = t ^ ((t >> 1) & 0x01010101u);
-    return (c * 0x01041040u) >> 24;                 // c0 | c1 << 2 | c2 << 4 | c3 << 6
-}
-// 4-bit mask of the bad bytes of x (bit b = byte b): the 0x01 bits of the nonzero-byte mask gathered
-// by one multiply (partial products land on distinct bits, none in 24..27 but the wanted four).
-__device__ __forceinline__ uint32_t bad4(uint32_t x) {
-    const uint32_t m = __vcmpne4(expect4(x, (x >> 1) & 0x03030303u), 0u) & 0x01010101u;
-    return (m * 0x01020408u) >> 24;
-}
-__device__ __forceinline__ uint32_t bad16(uint4 v) {
-    return bad4(v.x) | (bad4(v.y) << 4) | (bad4(v.z) << 8) | (bad4(v.w) << 12);
-}
-__device__ __forceinline__ bool valid_byte(uint8_t b) {
-    uint8_t y = b | 0x20;
-    return y == 'a' || y == 'c' || y == 'g' || y == 't';
-}
-
 // A warp packs 128 consecutive words (2048 bases) per iteration: for q = 0..3 lane l reads the 16
 // bytes of word 32q + l (one coalesced 512-byte load per q) and writes that word (a coalesced
 // 128-byte store per q).  Grid-stride over the padded word range.
@@ -70,16 +40,14 @@ __global__ void __launch_bounds__(256, PFAC_PACK_MINB) pack_kernel(const uint8_t
             for (int q = 0; q < 4; ++q) {
                 if constexpr (INV) {
                     uint32_t bq = 0;
-                    packed[wb + 32 * q + lane] = pack4(v[q].x, bq) | (pack4(v[q].y, bq) << 8) |
-                                                 (pack4(v[q].z, bq) << 16) | (pack4(v[q].w, bq) << 24);
-                    const uint32_t m = bq ? bad16(v[q]) : 0u;
+                    packed[wb + 32 * q + lane] = pack16(v[q].x, v[q].y, v[q].z, v[q].w, bq);
+                    const uint32_t m = (bq & kBadMask) ? bad16(v[q]) : 0u;
                     inv[wb + 32 * q + lane] = (uint16_t)m;
                     if (q < 2) mlo |= m << (16 * q);
                     else mhi |= m << (16 * (q - 2));
-                    bad |= bq;
-                } else {  // one accumulator: the integer pipe is this kernel's limit
-                    packed[wb + 32 * q + lane] = pack4(v[q].x, bad) | (pack4(v[q].y, bad) << 8) |
-                                                 (pack4(v[q].z, bad) << 16) | (pack4(v[q].w, bad) << 24);
+                    bad |= m;
+                } else {  // one residue accumulator (tested against kBadMask below)
+                    packed[wb + 32 * q + lane] = pack16(v[q].x, v[q].y, v[q].z, v[q].w, bad);
                 }
             }
         } else {
@@ -97,7 +65,7 @@ __global__ void __launch_bounds__(256, PFAC_PACK_MINB) pack_kernel(const uint8_t
                         word |= (t ^ (t >> 1)) << (2 * j);
                     }
                 }
-                bad |= m;
+                bad |= m ? 1u : 0u;  // bit 0 lies in kBadMask
                 packed[w] = word;
                 if (INV) {
                     inv[w] = (uint16_t)m;
@@ -106,6 +74,7 @@ __global__ void __launch_bounds__(256, PFAC_PACK_MINB) pack_kernel(const uint8_t
                 }
             }
         }
+        if (!INV) bad &= kBadMask;  // INV: bad already holds exact masks
         if (first_bad && !wdone && __any_sync(~0u, bad != 0)) {
             // rare (once per warp): this lane's first bad byte (its words ascend with q)
             uint32_t off = ~0u;
@@ -129,6 +98,40 @@ __global__ void __launch_bounds__(256, PFAC_PACK_MINB) pack_kernel(const uint8_t
             wdone = true;  // later iterations of this warp only see larger positions
         }
     }
+}
+
+// first_bad = pos_base + the first index < n_own whose barrier bit is set (UINT64_MAX if none): one
+// min-reduction per warp, one atomicMin per warp that saw a barrier.
+__global__ void first_bad_inv_kernel(const uint16_t *__restrict__ inv, uint64_t n_own, uint64_t pos_base,
+                                     uint64_t *first_bad) {
+    const uint64_t nw = (n_own + 15) / 16;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    unsigned long long best = ~0ull;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += stride) {
+        uint32_t m = inv[w];
+        if (w * 16 + 16 > n_own) m &= (1u << (n_own - w * 16)) - 1;
+        if (m) {
+            best = pos_base + w * 16 + (__ffs(m) - 1);
+            break;  // this thread's later words are larger
+        }
+    }
+    // 64-bit min over the warp: the high words first, then the low words among the lanes that tie
+    const uint32_t hi = __reduce_min_sync(~0u, (uint32_t)(best >> 32));
+    const uint32_t lo = __reduce_min_sync(~0u, (uint32_t)(best >> 32) == hi ? (uint32_t)best : ~0u);
+    if ((threadIdx.x & 31) == 0 && ((uint64_t)hi << 32 | lo) != ~0ull)
+        atomicMin(reinterpret_cast<unsigned long long *>(first_bad), ((unsigned long long)hi << 32) | lo);
+}
+
+int launch_first_bad_inv(const uint16_t *d_inv, uint64_t n_own, uint64_t pos_base, uint64_t *d_first_bad,
+                         void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, sizeof(uint64_t), st);
+    if (e != cudaSuccess || n_own == 0) return e;
+    const uint64_t nw = (n_own + 15) / 16;
+    uint64_t blocks = (nw + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    first_bad_inv_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_inv, n_own, pos_base, d_first_bad);
+    return cudaGetLastError();
 }
 
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,

@@ -76,6 +76,11 @@ struct MatchPlan {
     bool all_smem_bar = false; // the same three for the barrier-mode variant (BAR)
     uint32_t window_bar = 0;
     size_t smem_bar = 0;
+    bool txt_ok = false;       // the text-input variant (TXT) fits in shared memory
+    bool txt_pref = false;     // ... and is the faster choice for this automaton (plan_match)
+    bool all_smem_txt = false; // the same three for it
+    uint32_t window_txt = 0;
+    size_t smem_txt = 0;
     int sms = 0;
 };
 
@@ -131,6 +136,8 @@ void derive_host_image(pfac_automaton *a);
 // kernels.cu launchers (all asynchronous on `stream`); return cudaError_t as int.
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,
                 uint64_t *d_first_bad, uint16_t *d_inv, void *stream);
+int launch_first_bad_inv(const uint16_t *d_inv, uint64_t n_own, uint64_t pos_base, uint64_t *d_first_bad,
+                         void *stream);
 int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_t *d_inv, uint64_t n_own,
                  uint64_t n_avail, int32_t *d_out, void *stream);
 int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
@@ -140,7 +147,8 @@ uint64_t compact_workspace_bytes(uint64_t n);
 int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
-                         void *stream, bool list_only = false);
+                         void *stream, bool list_only = false, const uint8_t *d_text = nullptr,
+                         uint64_t *d_first_bad = nullptr);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
                   const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,

@@ -18,12 +18,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
-KERNELS = ["pack_kernel", "match_fused", "match_kernel", "compact_kernel", "match_bar"]
-ALG = {"pack_kernel": 1.25, "match_fused": 4.25, "match_kernel": 4.25, "compact_kernel": 4.0, "match_bar": 4.375}
-TITLES = {"pack_kernel": "pack_kernel", "match_fused": "match_kernel<FUSE=1> (match + compact, bench default)",
+KERNELS = ["match_text", "pack_kernel", "match_fused", "match_kernel", "compact_kernel", "match_bar"]
+ALG = {"match_text": 5.0, "pack_kernel": 1.25, "match_fused": 4.25, "match_kernel": 4.25, "compact_kernel": 4.0, "match_bar": 4.375}
+TITLES = {"match_text": "match_kernel<TXT=1> (pack + match + compact from ASCII, bench default)",
+          "pack_kernel": "pack_kernel (--path fused)", "match_fused": "match_kernel<FUSE=1> (match + compact, --path fused)",
           "match_kernel": "match_kernel<FUSE=0> (--path separate)", "compact_kernel": "compact_kernel (--path separate)",
           "match_bar": "match_kernel<FUSE=1, BAR=1> (--barriers 80: FASTA newlines + N gaps)"}
-TRAFFIC_KEY = {"pack_kernel": "pack", "match_fused": "match_fused", "match_kernel": "match",
+TRAFFIC_KEY = {"match_text": "match_text", "pack_kernel": "pack", "match_fused": "match_fused", "match_kernel": "match",
                "compact_kernel": "compact", "match_bar": "match_bar"}
 METRICS = [
     ("gpu__time_duration.sum", "duration"),

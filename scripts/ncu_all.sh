@@ -8,8 +8,9 @@ cap() {  # cap <kernel regex> <out name> <skip> <bench args...>
     -o gpurun_out/${name}_${tag} -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/ncu_${name}_${tag}.log 2>&1
 }
 # skip counts: the bench's probe pass launches pack + fused match once before the 3 warm-ups
-cap pack_kernel pack_kernel 4 "$@"
-cap match_kernel match_fused 4 "$@"
+cap match_kernel match_text 4 --path text "$@"
+cap pack_kernel pack_kernel 4 --path fused "$@"
+cap match_kernel match_fused 4 --path fused "$@"
 cap match_kernel match_kernel 4 --path separate "$@"
 cap compact_kernel compact_kernel 3 --path separate "$@"
-cap match_kernel match_bar 4 --barriers 80 "$@"
+cap match_kernel match_bar 4 --path fused --barriers 80 "$@"
