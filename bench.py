@@ -156,6 +156,21 @@ def oracle_sample(pats, text, n_own, target_s):
     return m, dt, len(pos)
 
 
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def oracle_threads(o, text, m, n, p):
+    """The oracle (as it stands) over [0, m) split into p disjoint position ranges, one thread each
+    (the C oracle runs outside the GIL: ctypes releases it).  Returns (seconds, matches)."""
+    from concurrent.futures import ThreadPoolExecutor
+    cuts = [m * i // p for i in range(p + 1)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(p) as ex:
+        res = list(ex.map(lambda i: len(o.match_list(text, cuts[i], cuts[i + 1], n=n)[0]), range(p)))
+    return time.perf_counter() - t0, sum(res)
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -164,29 +179,28 @@ def run_reference(args):
     cfg, pats, sh, n_total, text = workload(args, 1, 0)
     from oracle import Oracle
     o = Oracle(pats)
+    p = host_cores() if args.ref_cores == 0 else args.ref_cores
     # size one step's sample so that W + K steps take about args.ref_budget seconds in total
-    probe = min(sh.n_own, 2_000_000)
-    t0 = time.perf_counter()
-    o.match_list(text, 0, probe, n=len(text))
-    rate = probe / max(time.perf_counter() - t0, 1e-6)
+    probe = min(sh.n_own, 2_000_000 * p)
+    dt, _ = oracle_threads(o, text, probe, len(text), p)
+    rate = probe / max(dt, 1e-6)
     per_step = args.ref_budget / max(1, args.steps + args.warmup)
     m = int(min(sh.n_own, max(100_000, rate * per_step)))
     for _ in range(args.warmup):
-        o.match_list(text, 0, m, n=len(text))
+        oracle_threads(o, text, m, len(text), p)
     times = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        o.match_list(text, 0, m, n=len(text))
-        times.append(time.perf_counter() - t0)
+        times.append(oracle_threads(o, text, m, len(text), p)[0])
     t = sum(times) / len(times)
     v = m / t / 1e9
-    sample = f"first {m} positions of the {cfg.name} text per step (walks read up to maxlen-1 further)"
+    sample = (f"first {m} positions of the {cfg.name} text per step, split into {p} disjoint ranges on {p} "
+              f"threads (walks read up to maxlen-1 further)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Gbases/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args), "n_bases_per_step": m, "patterns": len(pats)},
-        "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": p, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "Gbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -422,7 +436,7 @@ def run_pfac(args):
                "steps": e_steps, "api": "pfac_scan_host (host memory in and out; wall clock, max over ranks)"}
 
     # ---- quick sanity against the oracle on rank 0 (window of out[]) + CPU baseline
-    cpu = None
+    cpu = cpu_all = None
     if rank == 0:
         from oracle import Oracle
         w = min(n_own, 200_000)
@@ -436,6 +450,13 @@ def run_pfac(args):
             cpu = {"value": m / dt / 1e9, "unit": "Gbases/s", "cores": 1, "kind": "oracle",
                    "sample": f"first {m} positions of this rank's {cfg.name} text, oracle O2 "
                              f"(plain C, 1 thread), {dt:.1f} s"}
+            # the same oracle on every host core (disjoint position ranges, one thread each)
+            p = host_cores()
+            from oracle import Oracle
+            m_all = int(min(n_own, m / dt * p * args.cpu_seconds / 2))
+            dt_all, _ = oracle_threads(Oracle(pats), text, m_all, n_avail, p)
+            cpu_all = {"value": m_all / dt_all / 1e9, "unit": "Gbases/s", "cores": p, "kind": "oracle",
+                       "sample": f"first {m_all} positions, {p} disjoint ranges on {p} threads, {dt_all:.1f} s"}
 
     if rank == 0:
         line = {
@@ -467,7 +488,7 @@ def run_pfac(args):
                                             if compact_ms > 0 else None)},
             "match_gbases_per_s_per_gpu": n_own / (match_ms * 1e-3) / 1e9,
             "build_ms": build_ms, "prepare_ms": prepare_ms, "gen_s": t_gen,
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all, "e2e": e2e,
             "gpu_launches": kernels_per_step * args.steps,
             "clocks": clocks.summary(),
         }
@@ -504,6 +525,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-budget", type=float, default=60.0, help="reference arm: total seconds")
+    ap.add_argument("--ref-cores", type=int, default=0, help="reference arm threads (0: every host core)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -366,14 +366,16 @@ int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64
         e = launch_match_compact(*im, a->k, nullptr, nullptr, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
                                  d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad);
     } else {  // two kernels through the workspace (unaligned text, or a halo too long for the plan)
+        // pack records the first bad index over the readable text; the fused kernel skips the barrier
+        // bits when there is none and writes the owned part of it to d_first_bad
         uint32_t *packed = reinterpret_cast<uint32_t *>(after);
         uint16_t *inv = reinterpret_cast<uint16_t *>(after + al16(pfac_packed_words(n_avail) * 4));
-        // first_bad over the owned range [0, n_own) only, from the barrier bits
-        e = launch_pack(d_text, n_avail, packed, pfac_packed_words(n_avail), nullptr, inv, stream);
-        if (!e && d_first_bad) e = launch_first_bad_inv(inv, n_own, pos_base, d_first_bad, stream);
+        uint64_t *bad_all = reinterpret_cast<uint64_t *>(after + al16(pfac_packed_words(n_avail) * 4) +
+                                                         al16(pfac_inv_words(n_avail) * 2));
+        e = launch_pack(d_text, n_avail, packed, pfac_packed_words(n_avail), bad_all, inv, stream);
         if (!e)
             e = launch_match_compact(*im, a->k, packed, inv, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
-                                     d_count, d_hist, d_workspace, stream, list_only);
+                                     d_count, d_hist, d_workspace, stream, list_only, nullptr, d_first_bad, bad_all);
     }
     return e ? cuda_fail(e, "pfac_match_text_async") : PFAC_OK;
 }

@@ -85,7 +85,10 @@ struct MatchArgs {
     uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
     CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
     const uint8_t *text;   // TXT: the ASCII text (n_avail bytes, 16-byte aligned)
-    uint64_t *first_bad;   // TXT (nullable): atomicMin of pos_base + the first owned non-ACGT index
+    uint64_t *first_bad;   // TXT (nullable): atomicMin of pos_base + the first owned non-ACGT index;
+                           // bad_all set: written once from *bad_all (the owned part of it)
+    const uint64_t *bad_all;  // BAR, packed input (nullable): pack's first bad index over the readable
+                              // text; UINT64_MAX = no barrier anywhere, the barrier bits are not read
 };
 
 // One T row (4 cells).  Branch row: child per base.  Chain row: flag|L, then L forced bases.
@@ -235,11 +238,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // slice schedule: strided over the grid, or (fused) a contiguous run per warp so that the warp's
     // matches come out in position order
     constexpr bool CONTIG = FUSE || kContiguousSchedule;
-    const uint64_t s_first = CONTIG ? gw * p.slices_per_warp : gw;
-    const uint64_t s_end = CONTIG ? (s_first + p.slices_per_warp < p.nslices ? s_first + p.slices_per_warp : p.nslices)
-                                  : p.nslices;
+    // contiguous runs balanced to within one slice: warp gw owns [gw*N/TW, (gw+1)*N/TW) (a ceil-sized
+    // run per warp would leave the last warps idle: cfg2 has 30.2 slices per warp)
+    const uint64_t s_first = CONTIG ? gw * p.nslices / TW : gw;
+    const uint64_t s_end = CONTIG ? (gw + 1) * p.nslices / TW : p.nslices;
     const uint64_t s_stride = CONTIG ? 1 : TW;
     constexpr bool DIRECT = PFAC_TEXT_DIRECT && !BAR;
+    // BAR over packed text: when pack found no bad byte at all, the barrier bits are never read
+    bool no_bar = false;
+    if constexpr (BAR && !TXT) {
+        if (p.bad_all) {
+            const uint64_t b = __ldcg(p.bad_all);  // written by the pack kernel before this launch
+            no_bar = b == ~0ull;
+            if (p.first_bad && blockIdx.x == 0 && tid == 0) *p.first_bad = b < p.n_own ? p.c.pos_base + b : ~0ull;
+        }
+    }
     auto issue = [&](uint64_t sl, uint32_t *dst, uint64_t *b) {
         if constexpr (DIRECT) return;
         if constexpr (TXT) {  // the 16-byte multiple part of the slice's readable bytes (the rest: lanes)
@@ -252,7 +265,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         const uint64_t w0 = sl * (kSlice / 16);
         const uint64_t left = p.avail_words - w0;
         const uint32_t nw = left < p.slice_words ? (uint32_t)left : p.slice_words;
-        if constexpr (BAR) {  // the barrier bits of the same bases ride on the same mbarrier
+        if (BAR && !no_bar) {  // the barrier bits of the same bases ride on the same mbarrier
             const uint32_t ni = (nw + 7) & ~7u;  // 16-byte multiple (the inv array is padded to 8 words)
             uint16_t *idst = dst == txt0 ? inv0 : inv1;
             mbar_expect_tx(b, nw * 4 + ni * 2);
@@ -282,7 +295,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     }
     if (lane == 0 && s_first < s_end) issue(s_first, txt0, &bar[0]);
     const Tab<CT, WIN> tb{sT, sF, reinterpret_cast<const CT *>(p.T), reinterpret_cast<const CT *>(p.F), p.window};
-    mbar_wait(tab_bar, 0);
+    if constexpr (!TXT) mbar_wait(tab_bar, 0);  // TXT: after packing the first slice (overlaps the load)
 
     uint32_t it = 0;
     uint64_t wcount = 0;   // fused: matches of this warp so far
@@ -359,7 +372,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
             __syncwarp();  // the ASCII buffer is free: fetch the next slice while this one is matched
             if (lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, txt0, &bar[0]);
-        } else if constexpr (BAR) {
+            if (it == 0) mbar_wait(tab_bar, 0);
+        } else if (BAR && !no_bar) {
             uint32_t any = 0;
             for (uint32_t w = lane; w < (lend + 15) / 16; w += 32) any |= inv[w];
             bar_slice = __any_sync(~0u, any) != 0;
@@ -761,6 +775,7 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.c = CompactArgs{};
     a.text = nullptr;
     a.first_bad = nullptr;
+    a.bad_all = nullptr;
 }
 
 template <typename CT, bool LIST>
@@ -862,9 +877,10 @@ int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_
 int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_packed, const uint16_t *d_inv,
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
-                         void *stream, bool list_only, const uint8_t *d_text, uint64_t *d_first_bad) {
+                         void *stream, bool list_only, const uint8_t *d_text, uint64_t *d_first_bad,
+                         const uint64_t *d_bad_all) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (d_text && d_first_bad) {
+    if (d_first_bad && (d_text || n_own == 0)) {
         cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, 8, st);
         if (e != cudaSuccess) return e;
     }
@@ -875,7 +891,8 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     if (d_text && !img.plan.txt_ok) return cudaErrorNotSupported;
     a.inv = d_inv;
     a.text = d_text;
-    a.first_bad = d_text ? d_first_bad : nullptr;
+    a.first_bad = d_text || d_bad_all ? d_first_bad : nullptr;
+    a.bad_all = d_text ? nullptr : d_bad_all;
     const MatchPlan &pl = img.plan;
     const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
     const uint64_t warps = grid * kMWarps;

@@ -100,40 +100,6 @@ __global__ void __launch_bounds__(256, PFAC_PACK_MINB) pack_kernel(const uint8_t
     }
 }
 
-// first_bad = pos_base + the first index < n_own whose barrier bit is set (UINT64_MAX if none): one
-// min-reduction per warp, one atomicMin per warp that saw a barrier.
-__global__ void first_bad_inv_kernel(const uint16_t *__restrict__ inv, uint64_t n_own, uint64_t pos_base,
-                                     uint64_t *first_bad) {
-    const uint64_t nw = (n_own + 15) / 16;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    unsigned long long best = ~0ull;
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += stride) {
-        uint32_t m = inv[w];
-        if (w * 16 + 16 > n_own) m &= (1u << (n_own - w * 16)) - 1;
-        if (m) {
-            best = pos_base + w * 16 + (__ffs(m) - 1);
-            break;  // this thread's later words are larger
-        }
-    }
-    // 64-bit min over the warp: the high words first, then the low words among the lanes that tie
-    const uint32_t hi = __reduce_min_sync(~0u, (uint32_t)(best >> 32));
-    const uint32_t lo = __reduce_min_sync(~0u, (uint32_t)(best >> 32) == hi ? (uint32_t)best : ~0u);
-    if ((threadIdx.x & 31) == 0 && ((uint64_t)hi << 32 | lo) != ~0ull)
-        atomicMin(reinterpret_cast<unsigned long long *>(first_bad), ((unsigned long long)hi << 32) | lo);
-}
-
-int launch_first_bad_inv(const uint16_t *d_inv, uint64_t n_own, uint64_t pos_base, uint64_t *d_first_bad,
-                         void *stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, sizeof(uint64_t), st);
-    if (e != cudaSuccess || n_own == 0) return e;
-    const uint64_t nw = (n_own + 15) / 16;
-    uint64_t blocks = (nw + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    first_bad_inv_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_inv, n_own, pos_base, d_first_bad);
-    return cudaGetLastError();
-}
-
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,
                 uint64_t *d_first_bad, uint16_t *d_inv, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;

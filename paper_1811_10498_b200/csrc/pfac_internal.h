@@ -136,8 +136,6 @@ void derive_host_image(pfac_automaton *a);
 // kernels.cu launchers (all asynchronous on `stream`); return cudaError_t as int.
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,
                 uint64_t *d_first_bad, uint16_t *d_inv, void *stream);
-int launch_first_bad_inv(const uint16_t *d_inv, uint64_t n_own, uint64_t pos_base, uint64_t *d_first_bad,
-                         void *stream);
 int launch_match(const DeviceImage &img, const uint32_t *d_packed, const uint16_t *d_inv, uint64_t n_own,
                  uint64_t n_avail, int32_t *d_out, void *stream);
 int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
@@ -148,7 +146,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only = false, const uint8_t *d_text = nullptr,
-                         uint64_t *d_first_bad = nullptr);
+                         uint64_t *d_first_bad = nullptr, const uint64_t *d_bad_all = nullptr);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
                   const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,
