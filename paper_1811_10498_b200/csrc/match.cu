@@ -181,7 +181,13 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
 #ifndef PFAC_CONTIG
 #define PFAC_CONTIG 1
 #endif
-constexpr bool kContiguousSchedule = PFAC_CONTIG;  // unfused kernel: contiguous slice runs per warp (A/B)
+constexpr bool kContiguousSchedule = PFAC_CONTIG;
+#ifndef PFAC_BALANCED
+#define PFAC_BALANCED 0  // A/B knob: 1 = runs balanced to within one slice (measured slower on cfg2)
+#endif
+#ifndef PFAC_SPW_PAD
+#define PFAC_SPW_PAD 0   // A/B knob: extra slices per warp run (probes the out[] stream spacing)
+#endif  // unfused kernel: contiguous slice runs per warp (A/B)
 #ifndef PFAC_DRAIN_IPL
 #define PFAC_DRAIN_IPL 1
 #endif
@@ -240,8 +246,14 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     constexpr bool CONTIG = FUSE || kContiguousSchedule;
     // contiguous runs balanced to within one slice: warp gw owns [gw*N/TW, (gw+1)*N/TW) (a ceil-sized
     // run per warp would leave the last warps idle: cfg2 has 30.2 slices per warp)
+#if PFAC_BALANCED
     const uint64_t s_first = CONTIG ? gw * p.nslices / TW : gw;
     const uint64_t s_end = CONTIG ? (gw + 1) * p.nslices / TW : p.nslices;
+#else
+    const uint64_t s_first = CONTIG ? gw * p.slices_per_warp : gw;
+    const uint64_t s_end = CONTIG ? (s_first + p.slices_per_warp < p.nslices ? s_first + p.slices_per_warp : p.nslices)
+                                  : p.nslices;
+#endif
     const uint64_t s_stride = CONTIG ? 1 : TW;
     constexpr bool DIRECT = PFAC_TEXT_DIRECT && !BAR;
     // BAR over packed text: when pack found no bad byte at all, the barrier bits are never read
@@ -896,7 +908,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     const MatchPlan &pl = img.plan;
     const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
     const uint64_t warps = grid * kMWarps;
-    a.slices_per_warp = (a.nslices + warps - 1) / warps;
+    a.slices_per_warp = (a.nslices + warps - 1) / warps + PFAC_SPW_PAD;
     CompactArgs &c = a.c;
     c.out = d_out;
     c.n = n_own;
