@@ -279,6 +279,28 @@ def _full_config(idx):
     assert (pos2[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
     assert (pid2[:len(epos)].cpu().numpy() == epid).all()
     del packed, ws
+    # the text-input call (pack fused into the kernel; the bench default where the plan takes it) in
+    # both of its paths, on the same full input: list, count, first_bad and the whole dense out[]
+    prev = os.environ.get("PFAC_TEXT_KERNEL")
+    try:
+        for mode in ("1", "0"):
+            os.environ["PFAC_TEXT_KERNEL"] = mode
+            ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
+            out3 = torch.empty(n, dtype=torch.int32, device=DEV)
+            bad = torch.zeros(1, dtype=torch.int64, device=DEV)
+            pos2.fill_(-1)
+            P.match_text_async(a, dtext, n, n, out3, pos2, pid2, cnt, ws, first_bad=bad)
+            torch.cuda.synchronize()
+            assert int(cnt.item()) == len(epos) and int(bad.item()) == -1
+            assert (pos2[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
+            assert (pid2[:len(epos)].cpu().numpy() == epid).all()
+            assert bool((out3 == out).all())
+            del out3, ws
+    finally:
+        if prev is None:
+            os.environ.pop("PFAC_TEXT_KERNEL", None)
+        else:
+            os.environ["PFAC_TEXT_KERNEL"] = prev
     # sampled out[] windows (every element, including the zeros)
     o = Oracle(pats)
     n = len(text)
