@@ -214,7 +214,7 @@ def run_pfac(args):
     import torch.distributed as dist
 
     import paper_1811_10498_b200 as P
-    from paper_1811_10498_b200.parallel import gather_matches
+    from paper_1811_10498_b200.parallel import gather_lists_async, list_buffer
 
     world, rank, local = dist_env()
     ndev = torch.cuda.device_count()
@@ -261,8 +261,13 @@ def run_pfac(args):
     pack()
     P.match_compact_async(a, packed, n_own, n_avail, out, pos[:0], pid[:0], count, ws, pos_base=sh.start, inv=inv)
     cap = int(count.item()) + 1024
-    pos = torch.empty(cap, dtype=torch.int64, device=dev)
-    pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    if world > 1:  # fixed-size list buffers: the same capacity on every rank
+        ct = torch.tensor([cap], dtype=torch.int64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(ct, op=dist.ReduceOp.MAX)
+        cap = int(ct.item())
+    # the rank's whole result in one buffer [count | pos[cap] | pid[cap]]: the kernel writes into it and
+    # one NCCL gather moves it (no host read of the count inside a step)
+    lbuf, count, pos, pid = list_buffer(cap, dev)
     stream = torch.cuda.current_stream(dev)
     fused = args.path in ("fused", "list", "text", "text-list")
     list_only = args.path in ("list", "text-list")
@@ -326,8 +331,7 @@ def run_pfac(args):
         if ev is not None:
             ev[4].record(st)
         if world > 1:
-            m = int(count.item())
-            gather_matches(pos, pid, min(m, cap), dst=0)
+            gather_lists_async(lbuf, dst=0)
 
     for _ in range(args.warmup):
         step()
@@ -419,8 +423,11 @@ def run_pfac(args):
 
         def e2e_step():
             _, _, mm = P.scan_host(a, h_text, pos=h_pos, pid=h_pid, device=local, n_own=n_own, pos_base=sh.start)
-            if world > 1:
-                gather_matches(pos, pid, min(int(count.item()), cap), dst=0)
+            if world > 1:  # this rank's host list into its list buffer, then the gather
+                count.fill_(mm)
+                pos[:mm].copy_(h_pos[:mm], non_blocking=True)
+                pid[:mm].copy_(h_pid[:mm], non_blocking=True)
+                gather_lists_async(lbuf, dst=0)
             return mm
 
         e2e_step()

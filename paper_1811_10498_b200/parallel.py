@@ -84,3 +84,47 @@ def gather_matches(pos, pid, count: int, group=None, dst: int = 0):
         return None, None, counts
     return (torch.cat([g[:k] for g, k in zip(gp, counts)]), torch.cat([g[:k] for g, k in zip(gi, counts)]),
             counts)
+
+
+# ----------------------------------------------------------------------------- sync-free gather
+def list_buffer(cap: int, device):
+    """One byte buffer holding a rank's whole result, [count int64 | pos int64[cap] | pid int32[cap]]
+    (padded to 16 B), and its (count, pos, pid) views: the match kernels write straight into it, and
+    one gather moves it -- no host read of the count inside a step."""
+    import torch
+    nbytes = (8 + 12 * cap + 15) // 16 * 16
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    count = buf[0:8].view(torch.int64)
+    pos = buf[8:8 + 8 * cap].view(torch.int64)
+    pid = buf[8 + 8 * cap:8 + 12 * cap].view(torch.int32)
+    return buf, count, pos, pid
+
+
+def gather_lists_async(buf, group=None, dst: int = 0):
+    """Gather every rank's list buffer (list_buffer) to rank `dst`: one NCCL gather of fixed-size
+    buffers, stream-ordered after the kernel that filled them (no host synchronisation).  Returns a
+    (world, nbytes) uint8 tensor on `dst`, None elsewhere.  gloo: staged through host memory."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    src = buf.cpu() if (dist.get_backend(group) == "gloo" and buf.is_cuda) else buf
+    out = torch.empty((world, src.numel()), dtype=torch.uint8, device=src.device) if rank == dst else None
+    dist.gather(src, list(out.unbind(0)) if out is not None else None, dst=dst, group=group)
+    if out is not None and out.device != buf.device:
+        out = out.to(buf.device)
+    return out
+
+
+def unpack_lists(gathered, cap: int):
+    """Rank-order concatenation of gathered list buffers: (pos int64, pid int32, counts).  Counts
+    above `cap` (a rank's list overflowed its buffer) raise: the caller must re-run with a larger cap."""
+    import torch
+    g = gathered.cpu()
+    counts = [int(x) for x in g[:, 0:8].contiguous().view(torch.int64).flatten().tolist()]
+    if any(c > cap for c in counts):
+        raise ValueError(f"a rank's match count exceeds the list capacity {cap}: {counts}")
+    pos = [g[r, 8:8 + 8 * cap].contiguous().view(torch.int64)[:c] for r, c in enumerate(counts)]
+    pid = [g[r, 8 + 8 * cap:8 + 12 * cap].contiguous().view(torch.int32)[:c] for r, c in enumerate(counts)]
+    return torch.cat(pos), torch.cat(pid), counts

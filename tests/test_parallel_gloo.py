@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 import pfac_datagen as gen
 from oracle import Oracle
-from paper_1811_10498_b200.parallel import gather_matches, shard
+from paper_1811_10498_b200.parallel import gather_lists_async, gather_matches, list_buffer, shard, unpack_lists
 
 
 def test_shard_bounds_cover_and_align():
@@ -72,4 +72,45 @@ def test_sharded_gather_equals_single_run(world):
     text = gen.plant(gen.iid_text(8, 0, n), 0, n, pats, 8)
     epos, epid = Oracle(pats).match_list(text)
     assert sum(counts) == len(epos) > 50
+    assert (gp == epos.astype(np.int64)).all() and (gi == epid).all()
+
+
+def _worker_buf(rank, world, port, n, q):
+    """The sync-free form: each rank's result in one list buffer, one gather of the buffers."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pats = gen.random_patterns(9, 120, 4, 25)
+        sh = shard(n, world, rank, max(len(p) for p in pats))
+        text = gen.plant(gen.iid_text(9, sh.start, sh.avail_end), sh.start, n, pats, 9)
+        pos, pid = Oracle(pats).match_list(text, 0, sh.n_own, n=sh.n_avail)
+        cap = 20_000  # the same on every rank (fixed-size buffers); each rank's list fits
+        buf, count, bpos, bpid = list_buffer(cap, "cpu")
+        count[0] = len(pos)  # what the match kernel writes on the GPU
+        bpos[:len(pos)] = torch.from_numpy(pos.astype(np.int64) + sh.start)
+        bpid[:len(pid)] = torch.from_numpy(pid.astype(np.int32))
+        g = gather_lists_async(buf, dst=0)
+        if rank == 0:
+            gp, gi, counts = unpack_lists(g, cap)
+            q.put((gp.numpy(), gi.numpy(), counts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_list_buffer_gather_equals_single_run():
+    world, n = 3, 400_000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_buf, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gp, gi, counts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pats = gen.random_patterns(9, 120, 4, 25)
+    text = gen.plant(gen.iid_text(9, 0, n), 0, n, pats, 9)
+    epos, epid = Oracle(pats).match_list(text)
+    assert sum(counts) == len(epos) > 50 and len(counts) == world
     assert (gp == epos.astype(np.int64)).all() and (gi == epid).all()
