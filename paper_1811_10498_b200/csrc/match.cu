@@ -181,6 +181,13 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
 #ifndef PFAC_CONTIG
 #define PFAC_CONTIG 1
 #endif
+#ifndef PFAC_ZERO_CONTIG
+#define PFAC_ZERO_CONTIG 1
+#endif
+#ifndef PFAC_P16
+#define PFAC_P16 0  // A/B knob: filter-path interior slices with 16 positions per lane (measured: cfg2 -1.4%, cfg3 +2.8%)
+#endif
+constexpr bool kP16 = PFAC_P16;
 constexpr bool kContiguousSchedule = PFAC_CONTIG;
 #ifndef PFAC_BALANCED
 #define PFAC_BALANCED 0  // A/B knob: 1 = runs balanced to within one slice (measured slower on cfg2)
@@ -452,7 +459,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         };
         // Queue this lane's alive positions (bit r*8+j of `am` = position r*256 + lane*8 + j), one per
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
-        auto push = [&](uint32_t am, uint32_t gbase) {
+        // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
+        auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3) {
             while (true) {
                 const uint32_t b = __ballot_sync(~0u, am != 0);
                 if (!b) break;
@@ -460,13 +468,39 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 if (am) {
                     const uint32_t bit = __ffs(am) - 1;
                     am &= am - 1;
-                    queue[qn + __popc(b & lt)] = (uint16_t)(gbase + (bit >> 3) * kSubN + lane * kP + (bit & 7));
+                    queue[qn + __popc(b & lt)] =
+                        (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
                 }
                 qn += __popc(b);
             }
             drain(0);
         };
-        if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K) && !(BAR && bar_slice)) {
+        if (FBM && kP16 && lown == kSlice && lend >= kSlice + 16 + 16 && !(BAR && bar_slice)) {
+            // interior slice, filter path, 16 positions per lane: one 64-bit window holds the 16
+            // K1-mers of a lane (25 bases), and the warp's zero stores are four contiguous 512-B runs
+#pragma unroll 1
+          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+            uint32_t am = 0;
+#pragma unroll
+            for (uint32_t r = 0; r < 2; ++r) {
+                const uint32_t q = hg * 64 + r * 32 + lane;  // l0 = 16 q
+                const uint64_t x64 = (((uint64_t)txt[q + 1]) << 32) | txt[q];
+                uint32_t m = 0;
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) {
+                    const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
+                    m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
+                }
+                if constexpr (!LIST) {
+                    const uint32_t z0 = hg * 1024 + r * 512 + lane * 4;
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) st_stream_v4(out + z0 + 128 * k, 0u, 0u, 0u, 0u);
+                }
+                am |= m << (r * 16);
+            }
+            push(am, hg * 1024, 4);
+          }
+        } else if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K) && !(BAR && bar_slice)) {
             // interior slice: every position owned, every K-mer (K1-mer, K2-mer) readable
 #pragma unroll 1
           for (uint32_t hg = 0; hg < kHalves; ++hg) {
@@ -486,9 +520,16 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
                         m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
                     }
-                    if constexpr (!LIST) {
+                    if constexpr (!LIST) {  // the sub-slice's zeros: every store is zeros, so the warp
+                        // writes two contiguous 512-B runs (A/B knob: each lane its own 8 positions)
+#if PFAC_ZERO_CONTIG
+                        const uint32_t z0 = hg * 1024 + r * kSubN + lane * 4;
+                        st_stream_v4(out + z0, 0u, 0u, 0u, 0u);
+                        st_stream_v4(out + z0 + 128, 0u, 0u, 0u, 0u);
+#else
                         st_stream_v4(out + l0, 0u, 0u, 0u, 0u);
                         st_stream_v4(out + l0 + 4, 0u, 0u, 0u, 0u);
+#endif
                     }
                     am |= m << (r * kP);
                 } else {
