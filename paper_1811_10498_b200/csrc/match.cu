@@ -515,10 +515,27 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint32_t q = l0 >> 4;
                     const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> ((l0 & 15) * 2);
                     uint32_t m = 0;
+                    if constexpr (PFAC_FMA_SHR && !TXT) {
+                    // the same lookups with the shifts on the FMA pipe (packed-input kernels: +3.5% on
+                    // cfg2; the text kernel, whose packing loads the ALU pipe differently, loses 2.5%):
+                    // positions 0-5 from the low word y, 6-7 from z = x64 >> 12; K1-mer j of src =
+                    // bits [2jj, 2jj + 2 K1) of it
+                    static_assert(kFBK == 10 && kP == 8, "window split assumes 10-mers and 8 positions");
+                    const uint32_t y = (uint32_t)x64, z = (uint32_t)(x64 >> 12);
+#pragma unroll
+                    for (uint32_t j = 0; j < kP; ++j) {
+                        const uint32_t src = j < 6 ? y : z, jj = j < 6 ? j : j - 6;
+                        const uint32_t a = shr_fma(src, 2 * jj + 3) & 0x1FFFCu;  // byte offset of the word
+                        const uint32_t w = *reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(sFB) + a);
+                        const uint32_t s = jj ? shr_fma(src, 2 * jj) : src;       // low 5 bits: the bit
+                        m |= ((w >> (s & 31)) & 1u) << j;
+                    }
+                    } else {
 #pragma unroll
                     for (uint32_t j = 0; j < kP; ++j) {
                         const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
                         m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
+                    }
                     }
                     if constexpr (!LIST) {  // the sub-slice's zeros: every store is zeros, so the warp
                         // writes two contiguous 512-B runs (A/B knob: each lane its own 8 positions)

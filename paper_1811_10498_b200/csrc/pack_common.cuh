@@ -19,6 +19,23 @@ PFAC_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
     return (uint32_t)(((uint64_t)a * b) >> 32);
 #endif
 }
+// x >> k (1 <= k <= 31) as IMAD.HI on the FMA pipe: the integer ALU pipe (LOP3/SHF/PRMT) is the busier
+// of the two half-rate pipes in these kernels (ncu: math_pipe_throttle), so shifts move across.
+#ifndef PFAC_FMA_SHR
+#define PFAC_FMA_SHR 1
+#endif
+#ifndef PFAC_FMA_PACK
+#define PFAC_FMA_PACK 0  // measured: pack16's shifts stay on the ALU pipe (pack kernel and text kernel)
+#endif
+PFAC_HD uint32_t shr_fma(uint32_t x, uint32_t k) {
+#if defined(__CUDA_ARCH__) && PFAC_FMA_SHR
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - k)));
+    return r;
+#else
+    return x >> k;
+#endif
+}
 PFAC_HD uint32_t byte_perm(uint32_t a, uint32_t b, uint32_t s) {  // PRMT, selectors < 8 only
 #if defined(__CUDA_ARCH__)
     return __byte_perm(a, b, s);
@@ -41,9 +58,14 @@ PFAC_HD uint32_t byte_perm(uint32_t a, uint32_t b, uint32_t s) {  // PRMT, selec
 //     0x11 term); so a byte is in ACGTacgt iff its byte of ((x|0x20) ^ 'a' ^ 0x11*isT) & 0xF9 is 0.
 // pack4f returns the gathered byte in bits 0-7 (garbage above) and ORs the residue into acc.
 PFAC_HD uint32_t pack4f(uint32_t x, uint32_t &acc) {
+#if PFAC_FMA_PACK
+    const uint32_t s1 = shr_fma(x, 1);
+    const uint32_t is_t = shr_fma(x, 2) & ~s1 & 0x01010101u;
+#else
     const uint32_t s1 = x >> 1;
-    const uint32_t c2 = (x ^ s1) & 0x06060606u;
     const uint32_t is_t = (x >> 2) & ~s1 & 0x01010101u;
+#endif
+    const uint32_t c2 = (x ^ s1) & 0x06060606u;
     acc |= ((x | 0x20202020u) ^ 0x61616161u) ^ (is_t * 0x11u);
     return umulhi32(c2, 0x82082000u);
 }
