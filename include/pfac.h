@@ -183,9 +183,11 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
  * pfac_match_list_async) on d_text[0..n_avail), positions [0, n_own), without the packed and
  * barrier-mask arrays in HBM.  Definition: out[i] = id of the longest pattern starting at i
  * (PAPER.md:91, :204-207); bytes outside ACGTacgt are barriers (reading R5).
- *   d_text     device, n_avail bytes (16-byte aligned for the one-kernel path; otherwise, or when
- *              the automaton's halo is too long for its shared-memory plan (max_len > ~112), the
- *              call runs the two-kernel GPU path through buffers in d_workspace -- same results)
+ *   d_text     device, n_avail bytes (16-byte aligned for the one-kernel path; otherwise, when
+ *              the automaton's halo is too long for its shared-memory plan (max_len > ~112), or
+ *              when the plan prefers it (automata over 2^20 rows: pfac_image_info().text_kernel;
+ *              environment PFAC_TEXT_KERNEL=0 / 1 forces never / whenever it fits), the call runs
+ *              pack -> fused kernel through buffers in d_workspace -- same results)
  *   d_out      device int32[n_own], 16-byte aligned, or NULL: list only (no dense out[])
  *   d_pos/d_pid/capacity/d_count/d_hist/pos_base: as pfac_match_compact_async
  *   d_first_bad (nullable, device uint64): pos_base + the first owned index (< n_own) whose byte
