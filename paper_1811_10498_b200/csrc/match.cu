@@ -515,9 +515,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint32_t q = l0 >> 4;
                     const uint64_t x64 = ((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> ((l0 & 15) * 2);
                     uint32_t m = 0;
-                    if constexpr (PFAC_FMA_SHR && !TXT) {
-                    // the same lookups with the shifts on the FMA pipe (packed-input kernels: +3.5% on
-                    // cfg2; the text kernel, whose packing loads the ALU pipe differently, loses 2.5%):
+                    if constexpr (PFAC_FMA_SHR && !TXT && !LIST) {
+                    // the same lookups with the shifts on the FMA pipe (packed-input dense kernels: +3.5%
+                    // on cfg2; the text kernel, whose packing loads the ALU pipe differently, loses 2.5%,
+                    // the compute-bound list-only kernel ~5%):
                     // positions 0-5 from the low word y, 6-7 from z = x64 >> 12; K1-mer j of src =
                     // bits [2jj, 2jj + 2 K1) of it
                     static_assert(kFBK == 10 && kP == 8, "window split assumes 10-mers and 8 positions");
