@@ -718,6 +718,9 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
         }
     }
+    // TXT: a warp that had no slice never waited for the table copy; no CTA may retire while its
+    // bulk copy into shared memory is in flight
+    if (TXT && it == 0) mbar_wait(tab_bar, 0);
     if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
         const uint64_t prefix = grid_prefix<kMWarps>(wcount, p.c.counts, p.c.d_count, s_wcount, s_woff);
         for (uint64_t i = lane; i < wstaged; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);

@@ -441,3 +441,43 @@ def test_scan_host_shard_window():
     pos, pid, m = P.scan_host(P.Automaton(pats), torch.from_numpy(text), n_own=250_001, pos_base=7)
     epos, epid = Oracle(pats).match_list(text, 0, 250_001, n=n)
     assert m == len(epos) and (pos.numpy() == epos.astype(np.int64) + 7).all() and (pid.numpy() == epid).all()
+
+
+def test_config2_fasta_full_text_kernel():
+    """The bench's --barriers 80 workload at full size (cfg2 text with a newline every 80 bases and
+    N gaps, reading R5) through the text call in both of its paths: the whole list, the first bad
+    index, and sampled out[] windows, against the oracle."""
+    cfg = gen.CONFIGS[2]
+    pats = gen.config_patterns(cfg)
+    text = gen.config_text(cfg, patterns=pats)
+    gen.add_barriers(text, cfg.seed, line=80, block=1 << 20, run_max=100_000, run_frac=0.2)
+    n = len(text)
+    a = P.Automaton(pats)
+    dtext = to_dev(text)
+    epos, epid = _oracle_list_parallel(pats, text)
+    bad_idx = int(np.nonzero(~np.isin(text[:1000], np.frombuffer(b"ACGTacgt", np.uint8)))[0][0])
+    o = Oracle(pats)
+    prev = os.environ.get("PFAC_TEXT_KERNEL")
+    try:
+        for mode in ("1", "0"):
+            os.environ["PFAC_TEXT_KERNEL"] = mode
+            out = torch.empty(n, dtype=torch.int32, device=DEV)
+            cap = len(epos) + 1024
+            pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
+            pid = torch.empty(cap, dtype=torch.int32, device=DEV)
+            cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+            bad = torch.zeros(1, dtype=torch.int64, device=DEV)
+            ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
+            P.match_text_async(a, dtext, n, n, out, pos, pid, cnt, ws, first_bad=bad)
+            torch.cuda.synchronize()
+            assert int(cnt.item()) == len(epos) and int(bad.item()) == bad_idx
+            assert (pos[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
+            assert (pid[:len(epos)].cpu().numpy() == epid).all()
+            for s in [0, n // 2 + 3, n - 90_001]:
+                assert (out[s:s + 90_000].cpu().numpy() == o.match(text, s, s + 90_000)).all()
+            del out, ws
+    finally:
+        if prev is None:
+            os.environ.pop("PFAC_TEXT_KERNEL", None)
+        else:
+            os.environ["PFAC_TEXT_KERNEL"] = prev
