@@ -279,7 +279,8 @@ def run_pfac(args):
     graph_error = None
     # text path: one kernel when the image's plan takes it (pfac_image_info.text_kernel), else pack +
     # first-bad scan + fused kernel inside the call
-    text_one = text_in and a.image_info(local)["text_kernel"] == 1 and d_text.data_ptr() % 16 == 0
+    text_variant = a.image_info(local)["text_kernel"] if text_in and d_text.data_ptr() % 16 == 0 else 0
+    text_one = text_variant in (1, 2)
     kernels_per_step = (1 if text_one else 3 if text_in else 2 if fused else 3) + (1 if args.all_matches else 0)
     if args.all_matches:  # every occurrence: size the output from a probe
         ws_e = torch.empty(P.expand_workspace_bytes(), dtype=torch.uint8, device=dev)
@@ -478,7 +479,8 @@ def run_pfac(args):
                        "matches_per_step": m_final, "image": a.image_info(local)},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
-                         "kernel": ("match_kernel<TXT=1> (pack + match + compact)" if text_one and not list_only else
+                         "kernel": ("match_kernel<TXT=1" + (", 1024-position slices" if text_variant == 2 else "") +
+                                    "> (pack + match + compact)" if text_one and not list_only else
                                     "match_kernel<TXT=1, list-only> (pack + match + list)" if text_one else
                                     "pack + match_kernel<FUSE=1,BAR=1> (two-kernel text path)" if text_in else
                                     "match_kernel<FUSE=1, list-only>" if list_only else

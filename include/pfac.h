@@ -185,8 +185,9 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
  * (PAPER.md:91, :204-207); bytes outside ACGTacgt are barriers (reading R5).
  *   d_text     device, n_avail bytes (16-byte aligned for the one-kernel path; otherwise, when
  *              the automaton's halo is too long for its shared-memory plan (max_len > ~112), or
- *              when the plan prefers it (automata over 2^20 rows: pfac_image_info().text_kernel;
- *              environment PFAC_TEXT_KERNEL=0 / 1 forces never / whenever it fits), the call runs
+ *              when the plan prefers it (pfac_image_info().text_kernel; environment
+ *              PFAC_TEXT_KERNEL=0 / 1 / 2 forces never / whenever it fits / its 1024-position-slice
+ *              form), the call runs
  *              pack -> fused kernel through buffers in d_workspace -- same results)
  *   d_out      device int32[n_own], 16-byte aligned, or NULL: list only (no dense out[])
  *   d_pos/d_pid/capacity/d_count/d_hist/pos_base: as pfac_match_compact_async
@@ -260,7 +261,8 @@ typedef struct {
     uint64_t smem_bytes;      /* dynamic shared memory per CTA of the match kernel */
     uint64_t l2_persist_bytes;/* access-policy window over J2 */
     uint64_t image_bytes;     /* device memory of the image */
-    uint32_t text_kernel;     /* 1: pfac_match_text_async runs the one-kernel path on aligned text */
+    uint32_t text_kernel;     /* pfac_match_text_async on aligned text: 0 = pack + fused kernel,
+                                 1 = one kernel, 2 = one kernel with 1024-position slices */
     uint32_t text_window_rows;/* rows staged in shared memory by that kernel */
 } pfac_image_info_t;
 int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out);

@@ -319,13 +319,18 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
 
 static uint64_t al16(uint64_t x) { return (x + 15) & ~15ull; }
 
-// Whether pfac_match_text_async runs the one-kernel path for this image: the plan's measured
-// preference (MatchPlan::txt_pref), overridden by PFAC_TEXT_KERNEL=0 (never) / 1 (whenever it fits).
-static bool text_kernel_for(const DeviceImage &im) {
+// Which path pfac_match_text_async runs for this image: 0 = pack -> fused kernel, 1 = the text kernel,
+// 2 = the text kernel with 1024-position slices.  The plan's measured preference (MatchPlan::txt_pref,
+// txt1k_pref), overridden by PFAC_TEXT_KERNEL=0 (never) / 1 (whenever one fits; 2048 slices first) /
+// 2 (1024 slices whenever they fit).
+static int text_kernel_for(const DeviceImage &im) {
     const char *e = getenv("PFAC_TEXT_KERNEL");  // read per call (tests switch it)
     const int env = e && *e ? atoi(e) : -1;
-    if (!im.K2 || !im.plan.txt_ok || env == 0) return false;
-    return env == 1 || im.plan.txt_pref;
+    const MatchPlan &pl = im.plan;
+    if (!im.K2 || env == 0) return 0;
+    if (env == 2) return pl.txt1k_ok ? 2 : 0;
+    if (env == 1) return pl.txt_ok ? 1 : pl.txt1k_ok ? 2 : 0;
+    return pl.txt_pref ? 1 : pl.txt1k_pref ? 2 : 0;
 }
 
 uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int list_only) {
@@ -362,9 +367,11 @@ int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64
     int32_t *out = list_only ? reinterpret_cast<int32_t *>(after) : d_out;
     if (list_only) after += al16(n_own * 4);
     int e;
-    if (text_kernel_for(*im) && aligned16(d_text)) {
+    const int tk = text_kernel_for(*im);
+    if (tk && aligned16(d_text)) {
         e = launch_match_compact(*im, a->k, nullptr, nullptr, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
-                                 d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad);
+                                 d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad, nullptr,
+                                 tk == 2);
     } else {  // two kernels through the workspace (unaligned text, or a halo too long for the plan)
         // pack records the first bad index over the readable text; the fused kernel skips the barrier
         // bits when there is none and writes the owned part of it to d_first_bad
@@ -704,8 +711,8 @@ int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out)
     out->smem_bytes = im->plan.smem;
     out->l2_persist_bytes = im->l2_persist_bytes;
     out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4 + h.FB.size() * 4;
-    out->text_kernel = text_kernel_for(*im) ? 1u : 0u;
-    out->text_window_rows = im->plan.window_txt;
+    out->text_kernel = (uint32_t)text_kernel_for(*im);
+    out->text_window_rows = out->text_kernel == 2 ? im->plan.window_txt1k : im->plan.window_txt;
     return PFAC_OK;
 }
 

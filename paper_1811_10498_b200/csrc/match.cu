@@ -206,17 +206,22 @@ constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared me
 static __host__ __device__ constexpr uint32_t inv_buf_words(uint32_t slice_words) {  // uint16, 16-B multiple
     return (slice_words + 8 + 7) & ~7u;
 }
-static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, bool bar = false, bool txt = false) {
+static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, bool bar = false, bool txt = false,
+                                                         uint32_t bm_words = kBmWords) {
     // TXT: ASCII staging (slice_words * 16 bytes) + ONE packed slice and barrier-bit buffer (the warp
     // packs a slice before it prefetches the next one's bytes, so the ASCII buffer is the double buffer)
-    return txt ? slice_words * 16 + (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4 +
+    return txt ? slice_words * 16 + (slice_words + 4) * 4 + 16 + kQCap * 2 + bm_words * 4 +
                      inv_buf_words(slice_words) * 2
-               : 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + kBmWords * 4 +  // text, mbarriers, queue, bitmap
+               : 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + bm_words * 4 +  // text, mbarriers, queue, bitmap
                      (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);          // BAR: the slice's barrier bits
 }
 
-template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false, bool TXT = false>
+template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false, bool TXT = false,
+          uint32_t SL = kSlice>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
+    // positions per slice (text kernel for large automata: 1024, which leaves L1 more room)
+    static_assert(SL % 1024 == 0 && SL <= 65536, "slice = whole 1024-position groups, u16 positions");
+    constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32;
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     CT *sT = reinterpret_cast<CT *>(smem + (FBM ? kFBBytes : NJ * sizeof(CT)));
     CT *sF = sT + (size_t)p.window * 4;
     uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + p.window);  // 16-byte aligned (W % 8 == 0)
-    const uint32_t WB = warp_bytes(p.slice_words, BAR, TXT);
+    const uint32_t WB = warp_bytes(p.slice_words, BAR, TXT, kBmWordsT);
     uint64_t *tab_bar = reinterpret_cast<uint64_t *>(wbase + kMWarps * WB);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(txt1 + p.slice_words + 4);
     uint16_t *queue = reinterpret_cast<uint16_t *>(bar + 2);
     uint32_t *bm = reinterpret_cast<uint32_t *>(queue + kQCap);  // fused: nonzero cells of the slice
-    uint16_t *inv0 = reinterpret_cast<uint16_t *>(bm + kBmWords);  // BAR: barrier bits of the slice
+    uint16_t *inv0 = reinterpret_cast<uint16_t *>(bm + kBmWordsT);  // BAR: barrier bits of the slice
     uint16_t *inv1 = TXT ? inv0 : inv0 + inv_buf_words(p.slice_words);
     const uint32_t lt = (1u << lane) - 1;
     __shared__ uint64_t s_wcount[kMWarps], s_woff[kMWarps];
@@ -275,13 +280,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     auto issue = [&](uint64_t sl, uint32_t *dst, uint64_t *b) {
         if constexpr (DIRECT) return;
         if constexpr (TXT) {  // the 16-byte multiple part of the slice's readable bytes (the rest: lanes)
-            const uint64_t b0 = sl * kSlice, left = p.n_avail - b0;
+            const uint64_t b0 = sl * kSliceT, left = p.n_avail - b0;
             const uint32_t nb = (uint32_t)(left < p.slice_words * 16ull ? left : p.slice_words * 16ull) & ~15u;
             mbar_expect_tx(b, nb);
             if (nb) bulk_g2s(asc, p.text + b0, nb, b);
             return;
         }
-        const uint64_t w0 = sl * (kSlice / 16);
+        const uint64_t w0 = sl * (kSliceT / 16);
         const uint64_t left = p.avail_words - w0;
         const uint32_t nw = left < p.slice_words ? (uint32_t)left : p.slice_words;
         if (BAR && !no_bar) {  // the barrier bits of the same bases ride on the same mbarrier
@@ -327,19 +332,19 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         const uint32_t buf = it & 1;
         if (!TXT && lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
             if (FUSE) {
-            for (uint32_t w = lane; w < kBmWords; w += 32) bm[w] = 0;
+            for (uint32_t w = lane; w < kBmWordsT; w += 32) bm[w] = 0;
             __syncwarp();
         }
         if constexpr (TXT) mbar_wait(&bar[0], it & 1);
         else if constexpr (!DIRECT) mbar_wait(&bar[buf], (it >> 1) & 1);
-        const uint32_t *txt = DIRECT ? p.packed + sl * (kSlice / 16) : (buf ? txt1 : txt0);
+        const uint32_t *txt = DIRECT ? p.packed + sl * (kSliceT / 16) : (buf ? txt1 : txt0);
         const uint16_t *inv = buf ? inv1 : inv0;
         (void)inv;
-        const uint64_t base = sl * kSlice;
+        const uint64_t base = sl * kSliceT;
         const uint64_t avail_left = p.n_avail - base;
         const uint32_t lend = avail_left < p.slice_words * 16ull ? (uint32_t)avail_left : p.slice_words * 16;
         const uint64_t own_left = p.n_own - base;
-        const uint32_t lown = own_left < kSlice ? (uint32_t)own_left : kSlice;
+        const uint32_t lown = own_left < kSliceT ? (uint32_t)own_left : kSliceT;
         int32_t *out = p.out + base;
         // BAR: does any readable base of this slice (owned range + halo) fail to be ACGT?
         bool bar_slice = false;
@@ -475,11 +480,11 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
             drain(0);
         };
-        if (FBM && kP16 && lown == kSlice && lend >= kSlice + 16 + 16 && !(BAR && bar_slice)) {
+        if (FBM && kP16 && lown == kSliceT && lend >= kSliceT + 16 + 16 && !(BAR && bar_slice)) {
             // interior slice, filter path, 16 positions per lane: one 64-bit window holds the 16
             // K1-mers of a lane (25 bases), and the warp's zero stores are four contiguous 512-B runs
 #pragma unroll 1
-          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+          for (uint32_t hg = 0; hg < kHalvesT; ++hg) {
             uint32_t am = 0;
 #pragma unroll
             for (uint32_t r = 0; r < 2; ++r) {
@@ -500,10 +505,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             }
             push(am, hg * 1024, 4);
           }
-        } else if (lown == kSlice && lend >= kSlice + kP - 1 + (FBM ? 16 : K) && !(BAR && bar_slice)) {
+        } else if (lown == kSliceT && lend >= kSliceT + kP - 1 + (FBM ? 16 : K) && !(BAR && bar_slice)) {
             // interior slice: every position owned, every K-mer (K1-mer, K2-mer) readable
 #pragma unroll 1
-          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+          for (uint32_t hg = 0; hg < kHalvesT; ++hg) {
             uint32_t am = 0;
 #pragma unroll kPh1Unroll
             for (uint32_t r = 0; r < 4; ++r) {
@@ -576,7 +581,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             // it is queued with the filter-flagged ones, and drain() bounds every walk at the next
             // barrier (reading R5: a non-ACGT byte has no transition).  Zeros are stored first.
 #pragma unroll 1
-          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+          for (uint32_t hg = 0; hg < kHalvesT; ++hg) {
             uint32_t am = 0;
 #pragma unroll 1
             for (uint32_t r = 0; r < 4; ++r) {
@@ -620,7 +625,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
           }
         } else if (FBM) {  // slice at the end of the text: every owned position goes through drain()
 #pragma unroll 1
-          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+          for (uint32_t hg = 0; hg < kHalvesT; ++hg) {
             uint32_t am = 0;
 #pragma unroll 1
             for (uint32_t r = 0; r < 4; ++r) {
@@ -633,7 +638,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
           }
         } else {
 #pragma unroll 1
-          for (uint32_t hg = 0; hg < kHalves; ++hg) {
+          for (uint32_t hg = 0; hg < kHalvesT; ++hg) {
             uint32_t am = 0;
 #pragma unroll 1
             for (uint32_t r = 0; r < 4; ++r) {
@@ -677,19 +682,19 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
         if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
             uint32_t any = 0;
-            for (uint32_t w = lane; w < kBmWords; w += 32) any |= bm[w];
+            for (uint32_t w = lane; w < kBmWordsT; w += 32) any |= bm[w];
             uint32_t cnt = 0;
             if (__any_sync(~0u, any)) {  // most slices have no match (cfg2: 0.5 per slice)
-                for (uint32_t w = lane; w < kBmWords; w += 32) cnt += __popc(bm[w]);
+                for (uint32_t w = lane; w < kBmWordsT; w += 32) cnt += __popc(bm[w]);
 #pragma unroll
                 for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
             }
             if (!cnt) {  // after a spill, list-only mode still needs this slice's (empty) bitmap
                 if (LIST && wstaged != wcount)
-                    for (uint32_t w = lane; w < kBmWords; w += 32) p.c.bitmap[sl * kBmWords + w] = 0u;
+                    for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = 0u;
             } else if (wstaged == wcount && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
 #pragma unroll 1
-                for (uint32_t w0 = 0; w0 < kBmWords; w0 += 32) {
+                for (uint32_t w0 = 0; w0 < kBmWordsT; w0 += 32) {
                     uint32_t w = bm[w0 + lane];
                     const uint32_t c = __popc(w);
                     uint32_t incl = c;
@@ -713,7 +718,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             } else {  // the staging area is full: spill the slice's bitmap, emit it after the prefix
                 if (wstaged == wcount) spill_rel = (uint32_t)(sl - s_first);
                 if (LIST)  // out[] is valid only at matches: keep the slice's bitmap
-                    for (uint32_t w = lane; w < kBmWords; w += 32) p.c.bitmap[sl * kBmWords + w] = bm[w];
+                    for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = bm[w];
                 wcount += cnt;
             }
         }
@@ -728,8 +733,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // (list-only: masked by the spilled slice bitmaps, the scratch holds values only at matches)
         if (wcount > wstaged) {
             const uint64_t spill_first = s_first + spill_rel;
-            const uint64_t lo = spill_first * kSlice < p.n_own ? spill_first * kSlice : p.n_own;
-            const uint64_t hi = s_end * kSlice < p.n_own ? s_end * kSlice : p.n_own;
+            const uint64_t lo = spill_first * kSliceT < p.n_own ? spill_first * kSliceT : p.n_own;
+            const uint64_t hi = s_end * kSliceT < p.n_own ? s_end * kSliceT : p.n_own;
             warp_stream(
                 p.c, lo, hi, prefix + wstaged,
                 [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); },
@@ -764,11 +769,13 @@ constexpr size_t kStaticSmemReserve = 1024;
 #ifndef PFAC_TXT_MAX_ROWS
 #define PFAC_TXT_MAX_ROWS (1u << 20)
 #endif
-constexpr uint32_t kTxtMaxRows = PFAC_TXT_MAX_ROWS;  // larger automata keep the two-kernel text path  // the fused kernel's static shared arrays (grid_prefix)
+constexpr uint32_t kTxtMaxRows = PFAC_TXT_MAX_ROWS;  // larger automata: the text kernel with small slices
+constexpr uint32_t kSliceSmall = 1024;  // the fused kernel's static shared arrays (grid_prefix)
 
 static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
-                         bool bar = false, bool txt = false) {
-    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt) + 16;
+                         bool bar = false, bool txt = false, uint32_t bm_words = kBmWords) {
+    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt, bm_words) +
+           16;
 }
 
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
@@ -820,24 +827,40 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     // shared memory (cfg5 -5%) or the rows are many and L1 caches them (cfg4, 5.4 M states: -12%;
     // the text buffers take that L1).
     pl.txt_pref = pl.txt_ok && !(pl.all_smem && !pl.all_smem_txt) && h.rows <= kTxtMaxRows;
+    // the text kernel with 1024-position slices (uint32 images): half the staging, so L1 keeps room for
+    // the rows of large automata (cfg4: 1.84 vs 2.16 ms for 2048-position slices, vs 1.92 for pack +
+    // fused); 2% slower on cfg2-like automata, so it serves only those the 2048 plan is not used for
+    pl.slice_words_1k = kSliceSmall / 16 + halo_words_for(h.K2 > h.K ? h.K2 : h.K, maxlen);
+    const size_t fixed_k = match_smem(table, pl.cell, 0, pl.slice_words_1k, true, true, kSliceSmall / 32) +
+                           kStaticSmemReserve;
+    pl.txt1k_ok = h.K2 != 0 && pl.cell == 4 && (size_t)optin >= fixed_k;
+    uint32_t wk = pl.txt1k_ok ? (uint32_t)(((size_t)optin - fixed_k) / (5 * pl.cell)) & ~7u : 0u;
+    if (wk < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wk) wk = 0;
+#ifdef PFAC_WINDOW_MAX
+    if (wk > (uint32_t)(PFAC_WINDOW_MAX)) wk = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
+#endif
+    pl.all_smem_txt1k = wk >= h.rows;
+    pl.window_txt1k = pl.all_smem_txt1k ? h.rows : wk;
+    pl.smem_txt1k = match_smem(table, pl.cell, pl.window_txt1k, pl.slice_words_1k, true, true, kSliceSmall / 32);
+    pl.txt1k_pref = pl.txt1k_ok && !pl.txt_pref && pl.txt_ok && h.rows > kTxtMaxRows;
     pl.sms = sms;
     return pl;
 }
 
 static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_packed, uint64_t n_own,
-                      uint64_t n_avail, int32_t *d_out) {
+                      uint64_t n_avail, int32_t *d_out, uint32_t slice = kSlice) {
     a.packed = d_packed;
     a.out = d_out;
     a.n_own = n_own;
     a.n_avail = n_avail;
-    a.nslices = (n_own + kSlice - 1) / kSlice;
+    a.nslices = (n_own + slice - 1) / slice;
     a.avail_words = ((n_avail + 15) / 16 + 3) & ~3ull;
     a.J = img.d_J;
     a.T = img.d_T;
     a.F = img.d_F;
     a.window = img.plan.window;
     a.root = img.root;
-    a.slice_words = img.plan.slice_words;
+    a.slice_words = slice == kSlice ? img.plan.slice_words : img.plan.slice_words_1k;
     a.short_pat = img.short_pat;
     a.bar_dead = (1u << (img.minlen < (uint32_t)kFBK ? img.minlen : (uint32_t)kFBK)) - 1;
     a.J2 = img.d_J2;
@@ -852,16 +875,20 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.bad_all = nullptr;
 }
 
-template <typename CT, bool LIST>
+template <typename CT, bool LIST, uint32_t SL = kSlice>
 static const void *txt_kernel(bool all_smem) {
-    return all_smem ? (const void *)match_kernel<CT, false, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true>
-                    : (const void *)match_kernel<CT, true, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true>;
+    return all_smem ? (const void *)match_kernel<CT, false, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL>
+                    : (const void *)match_kernel<CT, true, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL>;
 }
 
 template <bool FUSE>
-static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false, bool txt = false) {
+static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false, bool txt = false,
+                              bool small = false) {
     const MatchPlan &pl = img.plan;
     if constexpr (FUSE) {
+        if (txt && small)  // text input, 1024-position slices (uint32 images only)
+            return list ? txt_kernel<uint32_t, true, kSliceSmall>(pl.all_smem_txt1k)
+                        : txt_kernel<uint32_t, false, kSliceSmall>(pl.all_smem_txt1k);
         if (txt) {  // text input (filter path; checked by the launcher)
             if (pl.cell == 2) return list ? txt_kernel<uint16_t, true>(pl.all_smem_txt) : txt_kernel<uint16_t, false>(pl.all_smem_txt);
             return list ? txt_kernel<uint32_t, true>(pl.all_smem_txt) : txt_kernel<uint32_t, false>(pl.all_smem_txt);
@@ -898,10 +925,10 @@ static const void *kernel_for(const DeviceImage &img, bool bar, bool list = fals
 // Launch with the image's L2 access-policy window (J2 persisting in L2) and, for the fused kernel,
 // as a cooperative launch (every CTA resident: the grid-wide prefix spins on its predecessors).
 static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchArgs &a, bool cooperative,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool small = false) {
     const MatchPlan &pl = img.plan;
-    const size_t smem = a.text ? pl.smem_txt : a.inv ? pl.smem_bar : pl.smem;
-    if (a.text) a.window = pl.window_txt;
+    const size_t smem = a.text ? (small ? pl.smem_txt1k : pl.smem_txt) : a.inv ? pl.smem_bar : pl.smem;
+    if (a.text) a.window = small ? pl.window_txt1k : pl.window_txt;
     else if (a.inv) a.window = pl.window_bar;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -952,7 +979,8 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only, const uint8_t *d_text, uint64_t *d_first_bad,
-                         const uint64_t *d_bad_all) {
+                         const uint64_t *d_bad_all, bool small) {
+    small = small && d_text;  // 1024-position slices: the text kernel only
     cudaStream_t st = (cudaStream_t)stream;
     if (d_first_bad && (d_text || n_own == 0)) {
         cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, 8, st);
@@ -960,9 +988,10 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     }
     if (n_own == 0) return cudaMemsetAsync(d_count, 0, 8, st);
     MatchArgs a;
-    fill_args(a, img, d_packed, n_own, n_avail, d_out);
+    const uint32_t slice = small ? kSliceSmall : kSlice;
+    fill_args(a, img, d_packed, n_own, n_avail, d_out, slice);
     if ((d_inv || list_only || d_text) && !img.K2) return cudaErrorNotSupported;  // filter path only
-    if (d_text && !img.plan.txt_ok) return cudaErrorNotSupported;
+    if (d_text && !(small ? img.plan.txt1k_ok : img.plan.txt_ok)) return cudaErrorNotSupported;
     a.inv = d_inv;
     a.text = d_text;
     a.first_bad = d_text || d_bad_all ? d_first_bad : nullptr;
@@ -988,10 +1017,11 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.stage_pid = reinterpret_cast<uint32_t *>(c.stage_pos + entries);
     c.bitmap = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_workspace) + kGMax * 8 +
                                             ((entries * 12 + 15) & ~15ull));
-    c.chunk = a.slices_per_warp * kSlice;
+    c.chunk = a.slices_per_warp * slice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr), grid, a, true, st);
+    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr, small), grid, a, true,
+                  st, small);
 }
 
 }  // namespace pfac

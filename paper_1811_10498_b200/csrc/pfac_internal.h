@@ -78,6 +78,12 @@ struct MatchPlan {
     size_t smem_bar = 0;
     bool txt_ok = false;       // the text-input variant (TXT) fits in shared memory
     bool txt_pref = false;     // ... and is the faster choice for this automaton (plan_match)
+    bool txt1k_ok = false;     // the text kernel with 1024-position slices fits (uint32 images)
+    bool txt1k_pref = false;   // ... and is the choice (automata over kTxtMaxRows rows)
+    bool all_smem_txt1k = false;
+    uint32_t window_txt1k = 0;
+    uint32_t slice_words_1k = 0;
+    size_t smem_txt1k = 0;
     bool all_smem_txt = false; // the same three for it
     uint32_t window_txt = 0;
     size_t smem_txt = 0;
@@ -146,7 +152,8 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only = false, const uint8_t *d_text = nullptr,
-                         uint64_t *d_first_bad = nullptr, const uint64_t *d_bad_all = nullptr);
+                         uint64_t *d_first_bad = nullptr, const uint64_t *d_bad_all = nullptr,
+                         bool small = false);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
                   const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,

@@ -283,7 +283,7 @@ def _full_config(idx):
     # both of its paths, on the same full input: list, count, first_bad and the whole dense out[]
     prev = os.environ.get("PFAC_TEXT_KERNEL")
     try:
-        for mode in ("1", "0"):
+        for mode in ("1", "0", "2"):
             os.environ["PFAC_TEXT_KERNEL"] = mode
             ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
             out3 = torch.empty(n, dtype=torch.int32, device=DEV)

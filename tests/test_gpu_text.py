@@ -27,10 +27,11 @@ ACGT8 = np.frombuffer(b"ACGTacgt", np.uint8)
 U64MAX = (1 << 64) - 1
 
 
-@pytest.fixture(autouse=True, params=["1", "0"], ids=["one-kernel", "two-kernel"])
+@pytest.fixture(autouse=True, params=["1", "0", "2"], ids=["one-kernel", "two-kernel", "one-kernel-1k"])
 def text_kernel(request, monkeypatch):
     """Both paths of pfac_match_text_async: the one-kernel TXT instantiation and the pack + fused
-    kernel path the call takes for unaligned text or automata the policy keeps off TXT."""
+    kernel path the call takes for unaligned text or automata the policy keeps off TXT; "2": the text
+    kernel with 1024-position slices (uint32 images; uint16 ones take the two-kernel path)."""
     monkeypatch.setenv("PFAC_TEXT_KERNEL", request.param)
     return request.param
 
@@ -187,7 +188,9 @@ def test_text_policy_info():
     a = P.Automaton(SETS["cfg2like"]())
     info = a.image_info(0)
     import os
-    assert info["text_kernel"] == (1 if os.environ["PFAC_TEXT_KERNEL"] == "1" else 0)
+    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 0}[os.environ["PFAC_TEXT_KERNEL"]]  # uint16 image
+    b = P.Automaton(SETS["big32"]())  # uint32 image
+    assert b.image_info(0)["text_kernel"] == {"1": 1, "0": 0, "2": 2}[os.environ["PFAC_TEXT_KERNEL"]]
 
 
 def test_text_empty():
