@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     if (lane == 0 && s_first < s_end) issue(s_first, txt0, &bar[0]);
     const Tab<CT, WIN> tb{sT, sF, reinterpret_cast<const CT *>(p.T), reinterpret_cast<const CT *>(p.F), p.window};
     if constexpr (!TXT) mbar_wait(tab_bar, 0);  // TXT: after packing the first slice (overlaps the load)
+    bool pred_bar = false;  // TXT: the previous slice had a barrier (FASTA text: every slice has one)
 
     uint32_t it = 0;
     uint64_t wcount = 0;   // fused: matches of this warp so far
@@ -350,44 +351,82 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         bool bar_slice = false;
         if constexpr (TXT) {
             // Pack the slice (16 bases per lane and step, PAPER.md:120's 4-letter alphabet as 2-bit
-            // codes); bytes past the readable end pack as A.  The hot pass only learns whether a byte
-            // outside ACGTacgt exists; the rare exact pass writes the barrier bits (reading R5).
+            // codes); bytes past the readable end pack as A.  Two forms, chosen by whether the previous
+            // slice had a barrier (a byte outside ACGTacgt, reading R5):
+            //  * plain text: the hot pass only ORs the validity residues; a slice that turns out to
+            //    hold a barrier gets its exact barrier bits in a second pass over its bytes;
+            //  * FASTA-like text (barriers in every slice): each word keeps its four residues and a
+            //    nonzero one gives the word's barrier bits at once (badmask16) -- one pass.
             const uint32_t nb = lend & ~15u;  // bytes the TMA brought; [nb, lend) come from global
             uint32_t acc = 0;
-            for (uint32_t q = lane; q < p.slice_words + 4; q += 32) {
-                uint32_t word = 0;
-                if (q * 16 + 16 <= nb) {
-                    const uint4 v = *reinterpret_cast<const uint4 *>(asc + q * 16);
-                    word = pack16(v.x, v.y, v.z, v.w, acc);
-                } else if (q * 16 < lend) {
-                    for (uint32_t j = 0; j < 16 && q * 16 + j < lend; ++j) {
-                        const uint32_t i = q * 16 + j;
-                        const uint8_t b = i < nb ? asc[i] : p.text[base + i];
-                        acc |= valid_byte(b) ? 0u : 1u;
-                        word |= (((b >> 1) ^ (b >> 2)) & 3u) << (2 * j);
+            auto tail_word = [&](uint32_t q, uint32_t &word) -> uint32_t {  // bytes [nb, lend) of word q
+                uint32_t m = 0;
+                for (uint32_t j = 0; j < 16 && q * 16 + j < lend; ++j) {
+                    const uint32_t i = q * 16 + j;
+                    const uint8_t b = i < nb ? asc[i] : p.text[base + i];
+                    m |= valid_byte(b) ? 0u : 1u << j;
+                    word |= (((b >> 1) ^ (b >> 2)) & 3u) << (2 * j);
+                }
+                return m;
+            };
+            if (pred_bar) {
+                for (uint32_t q = lane; q < inv_buf_words(p.slice_words); q += 32) {
+                    uint32_t word = 0, m = 0;
+                    if (q * 16 + 16 <= nb) {
+                        const uint4 v = *reinterpret_cast<const uint4 *>(asc + q * 16);
+                        uint32_t r0, r1, r2, r3;
+                        const uint32_t h0 = pack4r(v.x, r0), h1 = pack4r(v.y, r1), h2 = pack4r(v.z, r2),
+                                       h3 = pack4r(v.w, r3);
+                        word = byte_perm(byte_perm(h0, h1, 0x0040u), byte_perm(h2, h3, 0x0040u), 0x5410u);
+                        if ((r0 | r1 | r2 | r3) & kBadMask) m = badmask16(r0, r1, r2, r3);
+                    } else if (q * 16 < lend) {
+                        m = tail_word(q, word);
+                    }
+                    acc |= m;
+                    if (q < p.slice_words + 4) txt0[q] = word;
+                    inv0[q] = (uint16_t)m;
+                }
+                bar_slice = __any_sync(~0u, acc != 0);
+            } else {
+                for (uint32_t q = lane; q < p.slice_words + 4; q += 32) {
+                    uint32_t word = 0;
+                    if (q * 16 + 16 <= nb) {
+                        const uint4 v = *reinterpret_cast<const uint4 *>(asc + q * 16);
+                        word = pack16(v.x, v.y, v.z, v.w, acc);
+                    } else if (q * 16 < lend) {
+                        acc |= tail_word(q, word) ? 1u : 0u;
+                    }
+                    txt0[q] = word;
+                }
+                bar_slice = __any_sync(~0u, (acc & kBadMask) != 0);
+                if (bar_slice) {  // exact barrier bits of every word of the slice
+                    for (uint32_t q = lane; q < inv_buf_words(p.slice_words); q += 32) {
+                        uint32_t m = 0, w = 0;
+                        if (q * 16 + 16 <= nb) {
+                            const uint4 v = *reinterpret_cast<const uint4 *>(asc + q * 16);
+                            uint32_t r0, r1, r2, r3;
+                            pack4r(v.x, r0), pack4r(v.y, r1), pack4r(v.z, r2), pack4r(v.w, r3);
+                            m = badmask16(r0, r1, r2, r3);
+                        } else if (q * 16 < lend) {
+                            m = tail_word(q, w);
+                        }
+                        inv0[q] = (uint16_t)m;
                     }
                 }
-                txt0[q] = word;
             }
-            bar_slice = __any_sync(~0u, (acc & kBadMask) != 0);
-            if (bar_slice) {
+            if (bar_slice && p.first_bad && !bad_done) {  // the first owned barrier, from the bits
+                __syncwarp();
                 uint32_t firstb = ~0u;
-                for (uint32_t q = lane; q < inv_buf_words(p.slice_words); q += 32) {
-                    uint32_t m = 0;
-                    if (q * 16 + 16 <= nb) {
-                        m = bad16(*reinterpret_cast<const uint4 *>(asc + q * 16));
-                    } else if (q * 16 < lend) {
-                        for (uint32_t j = 0; j < 16 && q * 16 + j < lend; ++j) {
-                            const uint32_t i = q * 16 + j;
-                            m |= valid_byte(i < nb ? asc[i] : p.text[base + i]) ? 0u : 1u << j;
-                        }
+                for (uint32_t q = lane; q * 16 < lown; q += 32) {
+                    const uint32_t m = inv0[q];
+                    const uint32_t mo = lown - q * 16 >= 16 ? m : m & ((1u << (lown - q * 16)) - 1);
+                    if (mo) {
+                        firstb = q * 16 + (__ffs(mo) - 1);  // q ascends per lane
+                        break;
                     }
-                    inv0[q] = (uint16_t)m;
-                    const uint32_t mo = q * 16 < lown ? (lown - q * 16 >= 16 ? m : m & ((1u << (lown - q * 16)) - 1)) : 0u;
-                    if (mo && firstb == ~0u) firstb = q * 16 + (__ffs(mo) - 1);  // q ascends per lane
                 }
                 firstb = __reduce_min_sync(~0u, firstb);
-                if (p.first_bad && !bad_done && firstb != ~0u) {
+                if (firstb != ~0u) {
                     if (lane == 0)
                         atomicMin(reinterpret_cast<unsigned long long *>(p.first_bad),
                                   (unsigned long long)(p.c.pos_base + base + firstb));
@@ -680,6 +719,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
           }
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
+        if constexpr (TXT) pred_bar = bar_slice;
         if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
             uint32_t any = 0;
             for (uint32_t w = lane; w < kBmWordsT; w += 32) any |= bm[w];

@@ -71,6 +71,24 @@ PFAC_HD uint32_t pack4f(uint32_t x, uint32_t &acc) {
 }
 // 16 bytes -> one packed word; acc & kBadMask != 0 iff one of the bytes is outside ACGTacgt.
 constexpr uint32_t kBadMask = 0xF9F9F9F9u;
+// pack4f with the residue returned instead of accumulated (the text kernel keeps the four residues
+// of a word to derive its exact barrier bits when one is nonzero).
+PFAC_HD uint32_t pack4r(uint32_t x, uint32_t &res) {
+    res = 0;
+    return pack4f(x, res);
+}
+// 4-bit mask (bit b = byte b) of the bytes whose residue is nonzero in its kBadMask bits: bit 7 of
+// ((y & 0x7F) + 0x7F) | y is set iff the byte y is nonzero (no carry leaves a byte), and one
+// multiply gathers the four bit-7s (partial products land on distinct bits, only the four wanted
+// ones in 24..27).
+PFAC_HD uint32_t badmask4(uint32_t r) {
+    const uint32_t y = r & kBadMask;
+    const uint32_t h = (((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y) & 0x80808080u;
+    return ((h >> 7) * 0x01020408u) >> 24;
+}
+PFAC_HD uint32_t badmask16(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    return badmask4(r0) | (badmask4(r1) << 4) | (badmask4(r2) << 8) | (badmask4(r3) << 12);
+}
 PFAC_HD uint32_t pack16(uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t &acc) {
     const uint32_t h0 = pack4f(x, acc), h1 = pack4f(y, acc), h2 = pack4f(z, acc), h3 = pack4f(w, acc);
     return byte_perm(byte_perm(h0, h1, 0x0040u), byte_perm(h2, h3, 0x0040u), 0x5410u);

@@ -9,3 +9,5 @@ timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests_${tag}.l
 timeout 900 python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err; cat gpurun_out/bench_${tag}.json
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_${tag}.json 2>&1; tail -1 gpurun_out/bench_ref_${tag}.json
 bash scripts/ncu_all.sh ${tag}
+# FASTA-like text through the default (text) path and the packed BAR path
+for p in text fused; do timeout 300 python bench.py --barriers 80 --path $p --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | grep '^{' >> gpurun_out/bench_barriers_${tag}.jsonl; done

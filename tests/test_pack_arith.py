@@ -20,6 +20,17 @@ HDR = os.path.join(ROOT, "paper_1811_10498_b200", "csrc", "pack_common.cuh")
 SRC = r'''
 #include <cstddef>
 #include "%s"
+extern "C" void bad_masks(const uint8_t *b, size_t groups, uint32_t *masks) {
+    for (size_t g = 0; g < groups; ++g) {
+        uint32_t r[4];
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = b[16 * g + 4 * k] | (b[16 * g + 4 * k + 1] << 8) | (b[16 * g + 4 * k + 2] << 16) |
+                               ((uint32_t)b[16 * g + 4 * k + 3] << 24);
+            pfac::pack4r(x, r[k]);
+        }
+        masks[g] = pfac::badmask16(r[0], r[1], r[2], r[3]);
+    }
+}
 extern "C" void pack_groups(const uint8_t *b, size_t groups, uint32_t *words, uint8_t *bad) {
     for (size_t g = 0; g < groups; ++g) {
         uint32_t v[4];
@@ -44,6 +55,7 @@ def lib():
     subprocess.check_call(["g++", "-O2", "-std=c++17", "-x", "c++", "-shared", "-fPIC", "-o", so, src])
     L = ctypes.CDLL(so)
     L.pack_groups.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
+    L.bad_masks.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     return L
 
 
@@ -88,3 +100,21 @@ def test_random_groups(lib):
     ew, ebad, valid = expected(groups)
     assert (bad == ebad).all()
     assert (words[~ebad] == ew[~ebad]).all()
+
+
+def test_exact_barrier_bits_from_residues(lib):
+    """badmask16: bit j set iff byte j of the group is outside ACGTacgt (the text kernel's barrier
+    bits, reading R5), for every byte value at every position and for random mixed groups."""
+    rng = np.random.default_rng(2)
+    acgt = np.frombuffer(b"ACGTacgt", np.uint8)
+    groups = acgt[rng.integers(0, 8, (256 * 16, 16))]
+    for p in range(16):
+        groups[p * 256:(p + 1) * 256, p] = np.arange(256)
+    alphabet = np.frombuffer(b"ACGTacgtNnRYKM-\n>", np.uint8)
+    groups = np.concatenate([groups, alphabet[rng.integers(0, len(alphabet), (100_000, 16))]])
+    g = np.ascontiguousarray(groups)
+    masks = np.zeros(len(g), np.uint32)
+    lib.bad_masks(g.ctypes.data, len(g), masks.ctypes.data)
+    invalid = ~np.isin(g, acgt)
+    expect = (invalid.astype(np.uint32) << np.arange(16, dtype=np.uint32)).sum(axis=1)
+    assert (masks == expect).all()
