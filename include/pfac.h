@@ -210,13 +210,13 @@ int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64
  * {(pos_base + i, out[i]) : out[i] != 0, i < n_own} of the ASCII text h_text[0..n_avail) (walks
  * read up to n_avail >= n_own: a shard and its halo) on CUDA device `device`.  The text is streamed
  * in chunks with a (max_len - 1)-base halo: the host-to-device copy of chunk c+1 runs on one stream
- * while chunk c is packed and matched + compacted (fused kernel) on another, and each chunk's list
- * is copied back into h_pos/h_pid at its offset.  Pinned h_text gives copy/compute overlap;
- * pageable memory works too.  Bytes outside ACGTacgt are barriers (reading R5): a chunk holding one
- * is re-run with the barrier kernel.  *first_bad (nullable) receives the index (relative to h_text)
- * of the first such byte read, or UINT64_MAX.  Returns PFAC_E_CAPACITY if count > capacity (the
- * first `capacity` entries are written and *count is the total), PFAC_E_NON_ACGT only for a barrier
- * on an image without the filter.  Synchronous.
+ * while chunk c goes through the text call (pfac_match_text_async: pack + match + compact in one
+ * kernel where the plan takes it) on another, and each chunk's list is copied back into h_pos/h_pid
+ * at its offset.  Pinned h_text gives copy/compute overlap; pageable memory works too.  Bytes
+ * outside ACGTacgt are barriers (reading R5).  *first_bad (nullable) receives the index (relative to
+ * h_text) of the first such byte at a position < n_own, or UINT64_MAX.  Returns PFAC_E_CAPACITY if
+ * count > capacity (the first `capacity` entries are written and *count is the total); PFAC_E_CUDA
+ * for images without the filter (PFAC_FB16=0 ablation builds).  Synchronous.
  */
 int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, uint64_t n_own,
                    uint64_t n_avail, uint64_t pos_base, uint64_t *h_pos, uint32_t *h_pid,

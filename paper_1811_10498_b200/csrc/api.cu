@@ -339,6 +339,11 @@ uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int l
            al16(pfac_packed_words(n_avail) * 4) + al16(pfac_inv_words(n_avail) * 2) + 16;
 }
 
+static int match_text_impl(const pfac_automaton *a, DeviceImage &imr, const uint8_t *d_text, uint64_t n_own,
+                           uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                           uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad,
+                           void *d_workspace, void *stream);
+
 int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64_t n_own, uint64_t n_avail,
                           int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
                           uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad, void *d_workspace,
@@ -361,6 +366,19 @@ int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64
     DeviceImage *im = nullptr;
     int rc = get_image(a, dev, &im);
     if (rc) return rc;
+    const int e = match_text_impl(a, *im, d_text, n_own, n_avail, d_out, pos_base, d_pos, d_pid, capacity, d_count,
+                                  d_hist, d_first_bad, d_workspace, stream);
+    return e ? cuda_fail(e, "pfac_match_text_async") : PFAC_OK;
+}
+
+// The text call's GPU work on one device image (pfac_match_text_async, pfac_scan_host's chunks):
+// the text kernel when the plan takes it and the text is 16-byte aligned, else pack -> fused kernel
+// through the workspace.  n_own > 0.  Returns a cudaError_t.
+static int match_text_impl(const pfac_automaton *a, DeviceImage &imr, const uint8_t *d_text, uint64_t n_own,
+                           uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                           uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad,
+                           void *d_workspace, void *stream) {
+    DeviceImage *im = &imr;
     uint8_t *ws = reinterpret_cast<uint8_t *>(d_workspace);
     const bool list_only = d_out == nullptr;
     uint8_t *after = ws + al16(compact_workspace_bytes(n_own));
@@ -384,7 +402,7 @@ int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64
             e = launch_match_compact(*im, a->k, packed, inv, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
                                      d_count, d_hist, d_workspace, stream, list_only, nullptr, d_first_bad, bad_all);
     }
-    return e ? cuda_fail(e, "pfac_match_text_async") : PFAC_OK;
+    return e;
 }
 
 int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
@@ -444,14 +462,11 @@ namespace pfac {
 // Device buffers of one pipeline slot of pfac_scan_host.
 struct ScanSlot {
     uint8_t *text = nullptr;
-    uint32_t *packed = nullptr;
-    uint16_t *inv = nullptr;  // per-word invalid-base masks (barrier mode, filter images only)
     int32_t *out = nullptr;
     uint64_t *pos = nullptr, *cnt = nullptr, *bad = nullptr;
     uint32_t *pid = nullptr;
-    void *ws = nullptr;
+    void *ws = nullptr;  // pfac_match_text_workspace_bytes(chunk, chunk + halo, 0)
     uint64_t cap = 0;
-    bool bar = false;  // this slot's chunk was matched with the barrier kernel
     cudaEvent_t h2d = nullptr, done = nullptr;
 };
 // pfac_scan_host's pipeline resources, kept with the device image and reused across calls.
@@ -464,8 +479,6 @@ struct ScanCtx {
     ~ScanCtx() {
         for (ScanSlot &sl : slot) {
             cudaFree(sl.text);
-            cudaFree(sl.packed);
-            cudaFree(sl.inv);
             cudaFree(sl.out);
             cudaFree(sl.pos);
             cudaFree(sl.pid);
@@ -484,18 +497,15 @@ struct ScanCtx {
         cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaMallocHost(&h_cnt, 4 * sizeof(uint64_t));
-        const uint64_t words = pfac_packed_words(chunk + halo);
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
             ScanSlot &sl = slot[i];
             sl.cap = chunk / 8 + 65536;
             e = cudaMalloc(&sl.text, chunk + halo + 16);
-            if (e == cudaSuccess) e = cudaMalloc(&sl.packed, words * 4);
-            if (e == cudaSuccess) e = cudaMalloc(&sl.inv, pfac_inv_words(chunk + halo) * 2);
             if (e == cudaSuccess) e = cudaMalloc(&sl.out, chunk * 4 + 16);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
             if (e == cudaSuccess) e = cudaMalloc(&sl.cnt, 16);
-            if (e == cudaSuccess) e = cudaMalloc(&sl.ws, compact_workspace_bytes(chunk));
+            if (e == cudaSuccess) e = cudaMalloc(&sl.ws, pfac_match_text_workspace_bytes(chunk, chunk + halo, 0));
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
             sl.bad = sl.cnt + 1;
@@ -546,10 +556,8 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     uint64_t *h_cnt = X.h_cnt;
     cudaError_t e = cudaSuccess;
     uint64_t total = 0, bad_at = ~0ull;
-    // Barrier kernel or not is predicted from the last chunk whose result is known (a FASTA text has
-    // barriers in every chunk); a chunk that was predicted barrier-free but holds one is re-run.
-    bool predict_bar = false;
-    // enqueue chunk c (copy in, pack, fused match + compact, count + first-bad back to pinned memory)
+    // enqueue chunk c (copy in, the text call -- pack + match + compact in one kernel where the plan
+    // takes it; barriers handled per slice --, count + first owned bad index back to pinned memory)
     auto enqueue = [&](uint64_t c) -> cudaError_t {
         ScanSlot &sl = slot[c & 1];
         const uint64_t s0 = c * chunk, own = (n - s0) < chunk ? (n - s0) : chunk;
@@ -559,13 +567,8 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
         if (r == cudaSuccess) r = cudaEventRecord(sl.h2d, xs);
         if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, sl.h2d, 0);
         if (r == cudaSuccess)
-            r = (cudaError_t)launch_pack(sl.text, avail, sl.packed, pfac_packed_words(avail), sl.bad,
-                                         im->K2 ? sl.inv : nullptr, cs);
-        sl.bar = predict_bar && im->K2;
-        if (r == cudaSuccess)
-            r = (cudaError_t)launch_match_compact(*im, a->k, sl.packed, sl.bar ? sl.inv : nullptr, own, avail,
-                                                  sl.out, pos_base + s0, sl.pos, sl.pid, sl.cap, sl.cnt, nullptr,
-                                                  sl.ws, cs);
+            r = (cudaError_t)match_text_impl(a, *im, sl.text, own, avail, sl.out, pos_base + s0, sl.pos, sl.pid,
+                                             sl.cap, sl.cnt, nullptr, sl.bad, sl.ws, cs);
         if (r == cudaSuccess) r = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 16, cudaMemcpyDeviceToHost, cs);
         if (r == cudaSuccess) r = cudaEventRecord(sl.done, cs);
         return r;
@@ -578,35 +581,25 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
         e = cudaEventSynchronize(sl.done);
         if (e != cudaSuccess) break;
         uint64_t m = h_cnt[2 * (c & 1)];
-        const uint64_t b = h_cnt[2 * (c & 1) + 1];
-        if (b != ~0ull && bad_at == ~0ull) bad_at = c * chunk + b;
-        predict_bar = b != ~0ull;
-        if (b != ~0ull && !im->K2) {
-            e = cudaErrorNotSupported;  // barrier semantics live on the filter path (PFAC_FB16=1)
-            break;
-        }
-        // Chunk with barrier bytes: redo it with the barrier kernel.  Dense chunk: grow this slot's
-        // list (kept for later calls) and redo it.  Both run after the next chunk's enqueue, which
-        // touches only the other slot.
+        const uint64_t b = h_cnt[2 * (c & 1) + 1];  // pos_base-relative, owned positions only
+        if (b != ~0ull && bad_at == ~0ull) bad_at = b - pos_base;
+        // Dense chunk: grow this slot's list (kept for later calls) and redo it, after the next
+        // chunk's enqueue (which touches only the other slot).
         const uint64_t own = c * chunk + chunk <= n ? chunk : n - c * chunk;
         const uint64_t avail = (N - c * chunk) < chunk + halo ? N - c * chunk : chunk + halo;
-        for (bool redo = b != ~0ull && !sl.bar; (redo || m > sl.cap) && e == cudaSuccess;) {
+        if (m > sl.cap && e == cudaSuccess) {
             e = cudaStreamSynchronize(cs);
-            if (m > sl.cap) {
-                cudaFree(sl.pos);
-                cudaFree(sl.pid);
-                sl.cap = m + 1024;
-                if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
-                if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
-            }
+            cudaFree(sl.pos);
+            cudaFree(sl.pid);
+            sl.cap = m + 1024;
+            if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
+            if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
             if (e == cudaSuccess)
-                e = (cudaError_t)launch_match_compact(*im, a->k, sl.packed, b != ~0ull ? sl.inv : nullptr, own, avail,
-                                                      sl.out, pos_base + c * chunk, sl.pos, sl.pid, sl.cap, sl.cnt,
-                                                      nullptr, sl.ws, cs);
+                e = (cudaError_t)match_text_impl(a, *im, sl.text, own, avail, sl.out, pos_base + c * chunk, sl.pos,
+                                                 sl.pid, sl.cap, sl.cnt, nullptr, sl.bad, sl.ws, cs);
             if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 8, cudaMemcpyDeviceToHost, cs);
             if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
             m = h_cnt[2 * (c & 1)];
-            redo = false;
         }
         if (e != cudaSuccess) break;
         const uint64_t take = total >= capacity ? 0 : (capacity - total < m ? capacity - total : m);
@@ -619,8 +612,6 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(xs);
-    if (e == cudaErrorNotSupported)
-        return fail(PFAC_E_NON_ACGT, "pfac_scan_host: non-ACGT text needs the filter image (PFAC_FB16=1)");
     if (e != cudaSuccess) return cuda_fail(e, "pfac_scan_host");
     *count = total;
     if (first_bad) *first_bad = bad_at;
