@@ -481,3 +481,41 @@ def test_config2_fasta_full_text_kernel():
             os.environ.pop("PFAC_TEXT_KERNEL", None)
         else:
             os.environ["PFAC_TEXT_KERNEL"] = prev
+
+
+@pytest.mark.skipif(bool(os.environ.get("PFAC_SKIP_FULL")), reason="PFAC_SKIP_FULL set (4.3 Gbase run)")
+def test_text_beyond_2pow32_positions():
+    """Maximum-size edge: a text longer than 2^32 bases (64-bit positions, slice indices and byte
+    offsets end to end) through the text call in both paths; the whole list against the oracle and
+    every out[] element of windows straddling 2^32 and at the end."""
+    n = (1 << 32) + 100_003
+    pats = gen.random_patterns(300, 1000, 20, 20)
+    text = gen.plant(gen.iid_text(300, 0, n), 0, n, pats, 300)
+    a = P.Automaton(pats)
+    dtext = to_dev(text)
+    epos, epid = _oracle_list_parallel(pats, text)
+    assert len(epos) > 1_000_000 and int(epos[-1]) > (1 << 32)
+    o = Oracle(pats)
+    prev = os.environ.get("PFAC_TEXT_KERNEL")
+    try:
+        for mode in ("1", "0"):
+            os.environ["PFAC_TEXT_KERNEL"] = mode
+            out = torch.empty(n, dtype=torch.int32, device=DEV)
+            cap = len(epos) + 1024
+            pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
+            pid = torch.empty(cap, dtype=torch.int32, device=DEV)
+            cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+            ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
+            P.match_text_async(a, dtext, n, n, out, pos, pid, cnt, ws, pos_base=3)
+            torch.cuda.synchronize()
+            assert int(cnt.item()) == len(epos)
+            assert (pos[:len(epos)].cpu().numpy() == epos.astype(np.int64) + 3).all()
+            assert (pid[:len(epos)].cpu().numpy() == epid).all()
+            for s in [(1 << 32) - 50_000, n - 60_001]:
+                assert (out[s:s + 60_000].cpu().numpy() == o.match(text, s, s + 60_000)).all()
+            del out, ws
+    finally:
+        if prev is None:
+            os.environ.pop("PFAC_TEXT_KERNEL", None)
+        else:
+            os.environ["PFAC_TEXT_KERNEL"] = prev
