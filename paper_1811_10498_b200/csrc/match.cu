@@ -64,7 +64,6 @@ constexpr uint32_t kSubN = 32 * kP;         // 256 positions per sub-slice
 #define PFAC_SLICE 2048
 #endif
 constexpr uint32_t kSlice = PFAC_SLICE;     // positions per warp slice (A/B knob; multiple of 1024)
-constexpr uint32_t kHalves = kSlice / 1024; // 1024-position groups (one 32-bit alive mask each)
 constexpr uint32_t kBmWords = kSlice / 32;  // words of the fused kernel's per-slice match bitmap
 static_assert(kSlice % 1024 == 0 && kSlice <= 65536, "slice = whole 1024-position groups, u16 positions");
 
