@@ -62,7 +62,8 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     // One allocation [J2 | T | F | J | FB] (256-byte aligned parts); the L2 access-policy window
     // covers the J2 prefix.
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t bJ2 = al(h.J2.size() * 4), bT = al(h.T.size()), bF = al(h.F.size()), bJ = al(h.J.size()),
+    // J2 and the chain-head row copies HR together form the L2-persisting prefix
+    const size_t bJ2only = al(h.J2.size() * 4), bJ2 = bJ2only + al(h.HR.size() * 4), bT = al(h.T.size()), bF = al(h.F.size()), bJ = al(h.J.size()),
                  bFB = al(h.FB.size() * 4), bC = al(a->prefix_dev.size() * 4),
                  bCF = al(a->prefix_flat.size() * 4);
     cudaError_t e = cudaSetDevice(device);
@@ -70,6 +71,7 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     if (e == cudaSuccess) {
         uint8_t *b = reinterpret_cast<uint8_t *>(im->d_base);
         im->d_J2 = h.K2 ? reinterpret_cast<uint32_t *>(b) : nullptr;
+        im->d_HR = h.HR.empty() ? nullptr : reinterpret_cast<const uint32_t *>(b + bJ2only);
         im->d_T = b + bJ2;
         im->d_F = b + bJ2 + bT;
         im->d_J = b + bJ2 + bT + bF;
@@ -86,6 +88,8 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
         if (e == cudaSuccess) e = cudaMemcpy(im->d_F, h.F.data(), h.F.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(im->d_J, h.J.data(), h.J.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess && h.K2) e = cudaMemcpy(im->d_J2, h.J2.data(), h.J2.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && !h.HR.empty())
+            e = cudaMemcpy(const_cast<uint32_t *>(im->d_HR), h.HR.data(), h.HR.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess && h.K2) e = cudaMemcpy(im->d_FB, h.FB.data(), h.FB.size() * 4, cudaMemcpyHostToDevice);
     }
     im->K2 = h.K2;

@@ -12,6 +12,7 @@
 //     answer F, and a jump table J over all K-mers that performs the first K steps of every walk.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "../../include/pfac.h"
 #include "pfac_internal.h"
@@ -335,6 +336,30 @@ void derive_host_image(pfac_automaton *a) {
                 s2 = t;
             }
             im.J2[x] = (d == K2) ? (0x80000000u | dev[s2]) : a->F[s2];
+        }
+        // uint32 images: a live walk's first row is its depth-K2 state's, and chain-major numbering
+        // scatters those rows over T (each head is followed by its run), so most are DRAM misses.
+        // Chain-head rows are copied into a compact array HR that sits next to J2 inside the
+        // L2-persisting window; cell 3 (unused in chain rows) holds the head's device id, and the
+        // J2 entry becomes ALIVE | HRF | index.  Branch heads keep pointing into T.
+        im.HR.clear();
+        if (cell == 4 && im.S < (1u << 30)) {
+            uint64_t heads = 0;
+            for (uint64_t x = 0; x < n2; ++x)
+                if (im.J2[x] & 0x80000000u) ++heads;
+            if (heads * 16 <= (8ull << 20)) {  // at most 8 MiB of copies
+                for (uint64_t x = 0; x < n2; ++x) {
+                    if (!(im.J2[x] & 0x80000000u)) continue;
+                    const uint32_t s = im.J2[x] & 0x7FFFFFFFu;
+                    uint32_t row[4];
+                    memcpy(row, im.T.data() + (size_t)s * 16, 16);
+                    if (!(row[0] & 0x80000000u)) continue;  // a branch row: stays in T
+                    row[3] = s;
+                    const uint32_t h = (uint32_t)(im.HR.size() / 4);
+                    im.HR.insert(im.HR.end(), row, row + 4);
+                    im.J2[x] = 0x80000000u | 0x40000000u | h;
+                }
+            }
         }
         // FB[x] = 1 iff the K1-mer x starts a walk that survives K1 bases or completes a pattern on the
         // way: every other position's answer is 0 without touching J2.

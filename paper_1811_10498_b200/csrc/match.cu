@@ -84,6 +84,7 @@ struct MatchArgs {
     uint64_t slices_per_warp;  // fused mode: each warp owns a contiguous run of slices
     CompactArgs c;         // fused mode: the match list (n = n_own, chunk = slices_per_warp * kSlice)
     const uint8_t *text;   // TXT: the ASCII text (n_avail bytes, 16-byte aligned)
+    const uint4 *HR;       // uint32 images (nullable): chain-head row copies, J2 entries ALIVE|HRF|index
     uint64_t *first_bad;   // TXT (nullable): atomicMin of pos_base + the first owned non-ACGT index;
                            // bad_all set: written once from *bad_all (the owned part of it)
     const uint64_t *bad_all;  // BAR, packed input (nullable): pack's first bad index over the readable
@@ -175,6 +176,29 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
         }
     }
     return tb.final_of(s);
+}
+
+// walk() from a depth-K2 chain head whose row comes from the compact copy HR (uint32 images): the
+// first step reads the given row (cell 3 = the head's device id), the rest continues in T.
+template <typename CT, bool WIN>
+__device__ __forceinline__ uint32_t walk_head(const Tab<CT, WIN> &tb, const uint32_t *txt, const uint4 row, uint32_t l,
+                                              uint32_t lend) {
+    const uint32_t s = row.w;
+    if (l >= lend) return tb.final_of(s);
+    Row<uint32_t> r;
+    r.r = row;
+    const uint32_t w = window16(txt, l);
+    const uint32_t L = r.len();
+    const uint32_t d = w ^ r.bits();
+    const uint32_t m = d ? (uint32_t)(__ffs(d) - 1) >> 1 : 16u;
+    const uint32_t rem = lend - l;
+    const uint32_t lim = L < rem ? L : rem;
+    if (m < lim || lim < L) {  // the walk ends inside this span
+        const uint32_t mm = m < lim ? m : lim;
+        if (r.nofin() || mm == 0) return r.fin();
+        return tb.final_of(s + mm);
+    }
+    return walk(tb, txt, s + L, l + L, lend);
 }
 
 #ifndef PFAC_CONTIG
@@ -481,6 +505,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         if (l[k] == 0xFFFFu) continue;
                         uint32_t res;
                         if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], le[k]);  // near the end / a barrier
+                        else if (sizeof(CT) == 4 && p.HR && (g[k] & 0x40000000u))  // a chain head's row copy
+                            res = walk_head(tb, txt, __ldg(p.HR + (g[k] & 0x3FFFFFFFu)), l[k] + p.K2, le[k]);
                         else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, le[k]);
                         else res = g[k];
                         if (!LIST || res) out[l[k]] = (int32_t)res;
@@ -912,6 +938,7 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.text = nullptr;
     a.first_bad = nullptr;
     a.bad_all = nullptr;
+    a.HR = reinterpret_cast<const uint4 *>(img.d_HR);
 }
 
 template <typename CT, bool LIST, uint32_t SL = kSlice>

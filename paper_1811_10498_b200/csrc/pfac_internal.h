@@ -64,6 +64,8 @@ struct HostImage {
     int K2 = 0;                        // uint32 images: second-level jump over K2-mers (0 = none)
     std::vector<uint32_t> J2;          // 4^K2 cells, same encoding as J (ALIVE = bit 31); L2-resident
     std::vector<uint32_t> FB;          // K2 > 0: 4^kFilterK-bit filter ("this K1-mer needs J2")
+    std::vector<uint32_t> HR;          // uint32 images: copies of the depth-K2 chain-head T rows (4 cells,
+                                       // cell 3 = the head's device id); J2 entry ALIVE|HRF|h points at row h
 };
 
 // Launch plan of the match kernel for one automaton on one device (match.cu).
@@ -106,6 +108,7 @@ struct DeviceImage {
     void *d_J = nullptr, *d_T = nullptr, *d_F = nullptr;  // cells of plan.cell bytes
     uint32_t *d_J2 = nullptr;                             // K2 > 0: L2-persisting second-level jump
     uint32_t *d_FB = nullptr;                             // K2 > 0: K1-mer filter bitmap
+    const uint32_t *d_HR = nullptr;                       // chain-head row copies, 4 cells each (or null)
     const uint32_t *d_prefix = nullptr;                   // prefix_dev (uint4 per pattern)
     const uint32_t *d_prefix_flat = nullptr;              // prefix_flat
     size_t l2_persist_bytes = 0;                          // access-policy window from d_base (0 = none)
