@@ -6,11 +6,15 @@ resident in HBM: pack (ASCII -> 2-bit) -> match (PFAC walk from every position) 
 list + count) [-> NCCL gather of counts and lists when N > 1].  Build (row 1) and the device image
 upload (row 2) happen once, before timing, and are reported as `build_ms` / `prepare_ms`.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--scaling weak|strong]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--scaling weak|strong]
   python bench.py --impl reference ...   # the oracle (CPU) on the same workload, bounded sample
 
-Default workload: BASELINE.json configs[1] (cfg2: 256 Mbp, 1000 patterns of length 20) per GPU,
-weak scaling (each rank owns one cfg2-sized shard of a longer text; halo maxlen-1).
+Default workload: N = 1: BASELINE.json configs[1] (cfg2: 256 Mbp, 1000 patterns of length 20), the
+config the metric is quoted on.  N > 1: configs[2] (cfg3: the 3.1 Gbp text, 10000 patterns of length
+16-64) split across the N ranks -- strong scaling, the north star's "near-linear 8-GPU scaling on
+the 3.1 Gbp config"; `--scaling weak` gives each rank a config-sized shard of a longer text instead.
+One process per GPU: under torchrun (WORLD_SIZE set) the ranks are torchrun's; `--gpus N` without
+WORLD_SIZE re-launches this script under torch.distributed.run with N ranks (127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
@@ -131,6 +135,44 @@ def workload(args, world, rank):
     return cfg, pats, sh, n_total, text
 
 
+def verify_gathered(args, gathered, cap, world, n_total, pats, window=200_000):
+    """Rank 0, after the warm-up (outside the timed region): the lists gathered from every rank
+    (parallel.unpack_lists) are in ascending global position, and for every rank the entries in the
+    first `window` owned positions equal the oracle's list of that window (text regenerated
+    position-addressably; cfg5's segment text is only regenerated for rank 0).  Returns a summary
+    dict; raises AssertionError on a mismatch (the bench then prints no line)."""
+    import numpy as np
+
+    import pfac_datagen as gen
+    from oracle import Oracle
+    from paper_1811_10498_b200.parallel import shard, unpack_lists
+    gp, gi, counts = unpack_lists(gathered, cap)
+    gp, gi = gp.numpy(), gi.numpy()
+    assert (np.diff(gp) > 0).all(), "gathered positions are not strictly ascending"
+    cfg = gen.CONFIGS[args.config]
+    maxlen = max(len(p) for p in pats)
+    o = Oracle(pats)
+    checked = 0
+    for r in range(world):
+        if cfg.repetitive and r > 0:
+            break
+        sh = shard(n_total, world, r, maxlen)
+        w = min(window, sh.n_own)
+        hi = min(n_total, sh.start + w + maxlen - 1)
+        if cfg.repetitive:
+            t = gen.config_text(cfg, 0, hi, patterns=pats, n=n_total)[sh.start:]
+        else:
+            t = gen.config_text(cfg, sh.start, hi, patterns=pats, n=n_total)
+        if args.barriers is not None:
+            gen.add_barriers(t, cfg.seed, line=args.barriers, a=sh.start, **BARRIER_GAPS)
+        ep, ei = o.match_list(t, 0, w, n=len(t))
+        sel = (gp >= sh.start) & (gp < sh.start + w)
+        assert (gp[sel] == ep.astype(np.int64) + sh.start).all() and (gi[sel] == ei).all(), f"rank {r} list differs"
+        checked += w
+    return {"ranks": world, "counts": counts, "total": int(sum(counts)), "ascending": True,
+            "oracle_checked_positions": checked}
+
+
 # assembly gaps for --barriers: in 20% of 1 Mbase blocks a run of up to 100 kbases of N (~1% of bytes)
 BARRIER_GAPS = {"block": 1 << 20, "run_max": 100_000, "run_frac": 0.2}
 
@@ -175,17 +217,31 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import pfac_datagen as gen  # noqa: F401
-    cfg, pats, sh, n_total, text = workload(args, 1, 0)
+    import pfac_datagen as gen
     from oracle import Oracle
+    cfg = gen.CONFIGS[args.config]
+    n_total = args.n or cfg.n  # the reference arm runs on one host: the whole text is its workload
+    pats = gen.config_patterns(cfg)
+    maxlen = max(len(p) for p in pats)
     o = Oracle(pats)
     p = host_cores() if args.ref_cores == 0 else args.ref_cores
+
+    def text_prefix(m):  # bases [0, m + maxlen - 1) of the workload's text (position-addressable)
+        hi = min(n_total, m + maxlen - 1)
+        t = gen.config_text(cfg, 0, hi, patterns=pats, n=n_total)
+        if args.barriers is not None:
+            gen.add_barriers(t, cfg.seed, line=args.barriers, **BARRIER_GAPS)
+        return t
+
     # size one step's sample so that W + K steps take about args.ref_budget seconds in total
-    probe = min(sh.n_own, 2_000_000 * p)
+    probe = min(n_total, 2_000_000 * p)
+    text = text_prefix(probe)
     dt, _ = oracle_threads(o, text, probe, len(text), p)
     rate = probe / max(dt, 1e-6)
     per_step = args.ref_budget / max(1, args.steps + args.warmup)
-    m = int(min(sh.n_own, max(100_000, rate * per_step)))
+    m = int(min(n_total, max(100_000, rate * per_step)))
+    if m > probe:
+        text = text_prefix(m)
     for _ in range(args.warmup):
         oracle_threads(o, text, m, len(text), p)
     times = []
@@ -198,7 +254,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Gbases/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args), "n_bases_per_step": m, "patterns": len(pats)},
         "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": p, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "Gbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -214,11 +270,16 @@ def run_pfac(args):
     import torch.distributed as dist
 
     import paper_1811_10498_b200 as P
-    from paper_1811_10498_b200.parallel import gather_lists_async, list_buffer
+    from paper_1811_10498_b200.parallel import gather_lists_async, list_buffer, unpack_lists
 
     world, rank, local = dist_env()
     ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise SystemExit("bench.py: no CUDA device visible (the PFAC path has no CPU fallback)")
     if world > 1:
+        if args.backend == "nccl" and world > ndev:
+            raise SystemExit(f"bench.py: {world} NCCL ranks need {world} GPUs, {ndev} visible "
+                             "(--backend gloo runs the ranks on shared GPUs, for tests only)")
         # --backend gloo + more ranks than GPUs exercises the N>1 control flow on one GPU (tests)
         local = local % ndev
         torch.cuda.set_device(local)
@@ -268,6 +329,7 @@ def run_pfac(args):
     # the rank's whole result in one buffer [count | pos[cap] | pid[cap]]: the kernel writes into it and
     # one NCCL gather moves it (no host read of the count inside a step)
     lbuf, count, pos, pid = list_buffer(cap, dev)
+    gathered = None
     stream = torch.cuda.current_stream(dev)
     fused = args.path in ("fused", "list", "text", "text-list")
     list_only = args.path in ("list", "text-list")
@@ -332,11 +394,15 @@ def run_pfac(args):
         if ev is not None:
             ev[4].record(st)
         if world > 1:
-            gather_lists_async(lbuf, dst=0)
+            return gather_lists_async(lbuf, dst=0)
+        return None
 
     for _ in range(args.warmup):
-        step()
+        gathered = step()
     torch.cuda.synchronize(dev)
+    gather_check = None
+    if world > 1:  # the gathered lists of the last warm-up step, checked on rank 0 (not timed)
+        gather_check = verify_gathered(args, gathered, cap, world, n_total, pats) if rank == 0 else None
     # sanity (not a parity claim; tests/ hold those): bad bytes only with --barriers, count fits,
     # first out[] window
     assert (int(bad.item()) == -1) != bars
@@ -475,6 +541,8 @@ def run_pfac(args):
             "config": {"workload": workload_name(cfg, args), "n_bases_total": n_total, "n_bases_per_rank": n_own,
                        "patterns": len(pats), "states": a.num_states, "max_len": a.max_len,
                        "parallelism": f"text-sharded x{world} (halo maxlen-1)",
+                       **({"ranks_per_gpu": -(-world // ndev), "backend": args.backend} if world > 1 else {}),
+                       **({"gather_check": gather_check} if gather_check else {}),
                        "l2": "inputs larger than L2 (no flush): ASCII text 1 B/base, out[] 4 B/base",
                        "matches_per_step": m_final, "image": a.image_info(local)},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
@@ -513,8 +581,11 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["pfac", "reference"], default="pfac")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--config", type=int, default=None, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default: 2 at N = 1, 3 at N > 1)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="N > 1: strong (default; the config's text split across the ranks) or weak "
+                         "(each rank a config-sized shard of an N-times longer text)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step's kernels directly instead of replaying one captured CUDA graph")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
@@ -538,7 +609,33 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:  # one process per GPU: re-launch under torch.distributed.run
+        return relaunch(args.gpus)
+    world = max(world, 1)
+    if world != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N ranks for --gpus N")
+    if args.config is None:
+        args.config = 2 if world == 1 else 3
+    if args.scaling is None:
+        args.scaling = "weak" if world == 1 else "strong"
     return run_reference(args) if args.impl == "reference" else run_pfac(args)
+
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N ...` without WORLD_SIZE: exec torch.distributed.run with N ranks on
+    this node (rendezvous on 127.0.0.1, a free port), forwarding every argument."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+    return 1  # not reached
 
 
 if __name__ == "__main__":

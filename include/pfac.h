@@ -14,10 +14,17 @@
  *    and pfac_last_error() then returns a thread-local message.
  *  - "d_" pointers are CUDA device pointers owned by the caller (e.g. torch tensors).  The device
  *    a call runs on is the one that owns its device buffers (found with cudaPointerGetAttributes),
- *    independent of any runtime's "current device".
+ *    independent of any runtime's "current device"; every call restores the calling thread's
+ *    current device before it returns.
  *  - `stream` is a cudaStream_t (CUstream) of that device, passed as void* so that this header
- *    needs no CUDA include.  "_async" calls only enqueue work on `stream`; the other compute calls
- *    synchronise `stream` before returning.
+ *    needs no CUDA include (the same pointer-sized handle; reading R18).  "_async" calls
+ *    only enqueue work on `stream`; the other compute calls return after completion (they
+ *    synchronise `stream`).
+ *  - L2 side effect: the first use of an automaton with a second-level jump table on a device
+ *    raises that device's cudaLimitPersistingL2CacheSize to the table's size (J2 + chain-head rows,
+ *    <= ~24 MiB; never lowered), and match launches mark that window persisting.  Co-resident
+ *    kernels of the same process see that much less normal L2; cudaCtxResetPersistingL2Cache
+ *    releases the lines.
  *  - Bases are the bytes A,C,G,T,a,c,g,t (case-insensitive; reading R4).
  */
 #ifndef PFAC_H
@@ -86,6 +93,10 @@ int pfac_prepare(const pfac_automaton *a, int device);
  * UINT64_MAX if there is none; codes of such bytes are unspecified.  Asynchronous.
  */
 uint64_t pfac_packed_words(uint64_t n);
+/* pfac_pack: the same, returning after completion.  first_bad (HOST, nullable)
+ * receives the first non-ACGTacgt index or UINT64_MAX; such a byte makes the call return
+ * PFAC_E_NON_ACGT (d_packed is still fully written; the codes of those bytes are unspecified). */
+int pfac_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *first_bad, void *stream);
 int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *d_first_bad,
                     void *stream);
 
@@ -107,6 +118,9 @@ int pfac_pack_barriers_async(const uint8_t *d_text, uint64_t n, uint32_t *d_pack
  */
 int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own,
                             uint64_t n_avail, int32_t *d_out, void *stream);
+/* The same, returning after completion (SURVEY.md Sec. 8(b) shard form). */
+int pfac_match_packed(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own,
+                      uint64_t n_avail, int32_t *d_out, void *stream);
 
 /* Match with barriers: as pfac_match_packed_async, and walks stop at every byte whose d_inv bit is
  * set (d_inv as written by pfac_pack_barriers_async for n_avail bases), so out[i] = 0 where text
@@ -117,13 +131,18 @@ int pfac_match_barriers_async(const pfac_automaton *a, const uint32_t *d_packed,
                               const uint16_t *d_inv, uint64_t n_own, uint64_t n_avail,
                               int32_t *d_out, void *stream);
 
-/* Convenience: pack + match over one ASCII text of n bytes (d_out: n int32).  Bytes outside
- * ACGTacgt are barriers (reading R5): the call packs with the barrier map, and only when the text
- * holds such a byte runs the barrier kernel.  *first_bad (host, nullable) receives the index of the
- * first such byte or UINT64_MAX.  PFAC_E_NON_ACGT only if the text has a barrier and the image has
- * no filter (PFAC_FB16=0 builds).  Synchronous. */
+/* pfac_match (one walk per character into an integer array):
+ * pack + match over one ASCII text of n bytes on the device (d_text: n bytes, any alignment; d_out:
+ * n int32, 16-byte aligned).  Bytes outside ACGTacgt are barriers (reading R5): the call packs with
+ * the barrier map, and only when the text holds such a byte runs the barrier kernel.  Returns after
+ * completion.  PFAC_E_NON_ACGT only if the text has a barrier and the image has no filter
+ * (PFAC_FB16=0 ablation builds). */
 int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out,
-               uint64_t *first_bad, void *stream);
+               void *stream);
+/* pfac_match that also reports the first barrier: *first_bad (HOST, nullable) receives the index
+ * of the first byte outside ACGTacgt, or UINT64_MAX.  Returns after completion. */
+int pfac_match_checked(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out,
+                       uint64_t *first_bad, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * Compact (step 5): the match list {(pos_base + i, out[i]) : out[i] != 0} in ascending i.
@@ -185,10 +204,9 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
  * (PAPER.md:91, :204-207); bytes outside ACGTacgt are barriers (reading R5).
  *   d_text     device, n_avail bytes (16-byte aligned for the one-kernel path; otherwise, when
  *              the automaton's halo is too long for its shared-memory plan (max_len > ~112), or
- *              when the plan prefers it (pfac_image_info().text_kernel; environment
- *              PFAC_TEXT_KERNEL=0 / 1 / 2 forces never / whenever it fits / its 1024-position-slice
- *              form), the call runs
- *              pack -> fused kernel through buffers in d_workspace -- same results)
+ *              when the plan prefers it (pfac_image_info().text_kernel; pfac_set_text_kernel
+ *              overrides the plan), the call runs pack -> fused kernel through buffers in
+ *              d_workspace -- same results)
  *   d_out      device int32[n_own], 16-byte aligned, or NULL: list only (no dense out[])
  *   d_pos/d_pid/capacity/d_count/d_hist/pos_base: as pfac_match_compact_async
  *   d_first_bad (nullable, device uint64): pos_base + the first owned index (< n_own) whose byte
@@ -200,6 +218,12 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
  * capacity is reported through *d_count > capacity (read it after a sync).
  */
 uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int list_only);
+/* Path policy of pfac_match_text_async for automaton `a` (all devices): mode -1 = the plan's
+ * measured choice (default), 0 = always pack -> fused kernel, 1 = the one-kernel path whenever it
+ * fits (2048-position slices first), 2 = its 1024-position-slice form whenever it fits.  Results
+ * are identical in every mode; only the kernels differ.  PFAC_E_ARG for other modes or a null a.
+ * The one mutable property of an automaton (an atomic; safe to change between calls). */
+int pfac_set_text_kernel(pfac_automaton *a, int mode);
 int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64_t n_own, uint64_t n_avail,
                           int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                           uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad,
@@ -259,11 +283,13 @@ typedef struct {
     uint32_t all_smem;        /* 1 if every row fits */
     uint32_t short_pat;       /* a pattern shorter than the jump length exists */
     uint64_t smem_bytes;      /* dynamic shared memory per CTA of the match kernel */
-    uint64_t l2_persist_bytes;/* access-policy window over J2 */
-    uint64_t image_bytes;     /* device memory of the image */
+    uint64_t l2_persist_bytes;/* access-policy window over J2 + the chain-head rows HR */
+    uint64_t image_bytes;     /* device memory of the image (all tables, HR and prefix chains) */
     uint32_t text_kernel;     /* pfac_match_text_async on aligned text: 0 = pack + fused kernel,
                                  1 = one kernel, 2 = one kernel with 1024-position slices */
     uint32_t text_window_rows;/* rows staged in shared memory by that kernel */
+    uint32_t hr_rows;         /* chain-head row copies next to J2 (uint32 images; 0 = none) */
+    uint32_t reserved;
 } pfac_image_info_t;
 int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out);
 

@@ -33,7 +33,14 @@ _SIGS = {
     "pfac_match_packed_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                                ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_match": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
-                                  ctypes.c_void_p, ctypes.c_void_p]),
+                                  ctypes.c_void_p]),
+    "pfac_match_checked": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_pack": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_void_p]),
+    "pfac_match_packed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_void_p, ctypes.c_void_p]),
+    "pfac_set_text_kernel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "pfac_compact_workspace_bytes": (ctypes.c_uint64, [ctypes.c_uint64]),
     "pfac_compact_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32,
@@ -107,7 +114,8 @@ class ImageInfo(ctypes.Structure):
                 ("K2", ctypes.c_uint32), ("states", ctypes.c_uint32), ("window_rows", ctypes.c_uint32),
                 ("all_smem", ctypes.c_uint32), ("short_pat", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint64),
                 ("l2_persist_bytes", ctypes.c_uint64), ("image_bytes", ctypes.c_uint64),
-                ("text_kernel", ctypes.c_uint32), ("text_window_rows", ctypes.c_uint32)]
+                ("text_kernel", ctypes.c_uint32), ("text_window_rows", ctypes.c_uint32),
+                ("hr_rows", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class PfacError(RuntimeError):
@@ -143,14 +151,28 @@ def _flatten(patterns) -> tuple[np.ndarray, np.ndarray]:
     return data, offs
 
 
-class Automaton:
-    """pfac_build(patterns): the BFS-ordered automaton, finals numbered as pattern ids."""
+# pfac_set_text_kernel mode applied to every new Automaton when its text_kernel argument is None
+# (None: the library's default, the plan's choice).  Tests switch it to cover every text path.
+DEFAULT_TEXT_KERNEL = None
 
-    def __init__(self, patterns):
+
+class Automaton:
+    """pfac_build(patterns): the BFS-ordered automaton, finals numbered as pattern ids.
+    text_kernel: pfac_set_text_kernel mode (-1 plan, 0 two kernels, 1 one kernel, 2 one kernel with
+    1024-position slices); None = DEFAULT_TEXT_KERNEL."""
+
+    def __init__(self, patterns, text_kernel=None):
         data, offs = _flatten(patterns)
         h = ctypes.c_void_p()
         _check(lib().pfac_build(data.ctypes.data, offs.ctypes.data, len(offs) - 1, ctypes.byref(h)))
         self._h = h
+        mode = DEFAULT_TEXT_KERNEL if text_kernel is None else text_kernel
+        if mode is not None:
+            self.set_text_kernel(mode)
+
+    def set_text_kernel(self, mode: int) -> None:
+        """pfac_set_text_kernel: the path policy of match_text_async for this automaton."""
+        _check(lib().pfac_set_text_kernel(self._h, int(mode)))
 
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:
@@ -255,13 +277,50 @@ def match_packed_async(a: Automaton, packed, n_own: int, n_avail: int | None = N
 
 
 def match(a: Automaton, text, out=None, stream=None):
-    """pfac_match: ASCII CUDA tensor -> int32 out (synchronous; non-ACGT bytes are barriers)."""
+    """pfac_match: ASCII CUDA tensor -> int32 out (returns after completion; non-ACGT bytes are barriers)."""
+    import torch
+    n = text.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=text.device)
+    _check(lib().pfac_match(a.handle, _ptr(text), n, _ptr(out), _stream(stream, text.device)))
+    return out
+
+
+def match_checked(a: Automaton, text, out=None, stream=None):
+    """pfac_match_checked: as match(), also returning the first non-ACGT index (-1 if none)."""
     import torch
     n = text.numel()
     if out is None:
         out = torch.empty(n, dtype=torch.int32, device=text.device)
     bad = ctypes.c_uint64(0)
-    _check(lib().pfac_match(a.handle, _ptr(text), n, _ptr(out), ctypes.byref(bad), _stream(stream, text.device)))
+    _check(lib().pfac_match_checked(a.handle, _ptr(text), n, _ptr(out), ctypes.byref(bad),
+                                    _stream(stream, text.device)))
+    return out, (-1 if bad.value == (1 << 64) - 1 else int(bad.value))
+
+
+def pack(text, packed=None, stream=None):
+    """pfac_pack (returns after completion): (packed, first_bad) with first_bad -1 if every byte is
+    ACGTacgt.  A non-ACGT byte is not an error here: the library's PFAC_E_NON_ACGT is returned as
+    first_bad >= 0 (the packed codes of such bytes are unspecified)."""
+    import torch
+    n = text.numel()
+    if packed is None:
+        packed = torch.empty(packed_words(n), dtype=torch.int32, device=text.device)
+    bad = ctypes.c_uint64(0)
+    rc = lib().pfac_pack(_ptr(text), n, _ptr(packed), ctypes.byref(bad), _stream(stream, text.device))
+    if rc != E_NON_ACGT:
+        _check(rc)
+    return packed, (-1 if bad.value == (1 << 64) - 1 else int(bad.value))
+
+
+def match_packed(a: Automaton, packed, n_own: int, n_avail: int | None = None, out=None, stream=None):
+    """pfac_match_packed: as match_packed_async, returning after completion."""
+    import torch
+    n_avail = n_own if n_avail is None else n_avail
+    if out is None:
+        out = torch.empty(n_own, dtype=torch.int32, device=packed.device)
+    _check(lib().pfac_match_packed(a.handle, _ptr(packed), n_own, n_avail, _ptr(out),
+                                   _stream(stream, packed.device)))
     return out
 
 

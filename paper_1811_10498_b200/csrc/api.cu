@@ -24,6 +24,23 @@ static int cuda_fail(int e, const char *where) {
     return fail(e == cudaErrorMemoryAllocation ? PFAC_E_OOM : PFAC_E_CUDA, msg);
 }
 
+// Restores the calling thread's current device on scope exit: entry points switch to the device that
+// owns their buffers and must not leave it current for the caller (pfac.h conventions).
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
 // Make the device that owns `p` current for this runtime on this thread (torch's runtime and ours
 // keep separate "current device" state).  Returns the device or -1 if p is not device memory.
 static int device_of(const void *p) {
@@ -158,6 +175,7 @@ uint32_t pfac_max_len(const pfac_automaton *a) { return a ? a->maxlen : 0; }
 const uint32_t *pfac_table(const pfac_automaton *a) { return a ? a->table.data() : nullptr; }
 
 int pfac_prepare(const pfac_automaton *a, int device) {
+    DeviceGuard guard;
     if (!a) return fail(PFAC_E_ARG, "pfac_prepare: null automaton");
     DeviceImage *im = nullptr;
     return get_image(a, device, &im);
@@ -166,6 +184,7 @@ int pfac_prepare(const pfac_automaton *a, int device) {
 uint64_t pfac_packed_words(uint64_t n) { return (((n + 15) / 16) + 3) & ~3ull; }
 
 int pfac_pack_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *d_first_bad, void *stream) {
+    DeviceGuard guard;
     if (n == 0) {  // nothing to pack; still report "no bad byte"
         if (!d_first_bad) return PFAC_OK;
         if (device_of(d_first_bad) < 0) return fail(PFAC_E_ARG, "pfac_pack_async: d_first_bad is not device memory");
@@ -183,6 +202,7 @@ uint64_t pfac_inv_words(uint64_t n) { return (pfac_packed_words(n) + 7) & ~7ull;
 
 int pfac_pack_barriers_async(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint16_t *d_inv,
                              uint64_t *d_first_bad, void *stream) {
+    DeviceGuard guard;
     if (!d_inv) return fail(PFAC_E_ARG, "pfac_pack_barriers_async: null d_inv");
     if (n == 0) return pfac_pack_async(d_text, n, d_packed, d_first_bad, stream);
     if (!d_packed || !d_text) return fail(PFAC_E_ARG, "pfac_pack_barriers_async: null buffer");
@@ -195,6 +215,7 @@ int pfac_pack_barriers_async(const uint8_t *d_text, uint64_t n, uint32_t *d_pack
 
 int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
                             int32_t *d_out, void *stream) {
+    DeviceGuard guard;
     if (!a) return fail(PFAC_E_ARG, "pfac_match_packed_async: null automaton");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_packed_async: n_avail < n_own");
     if (n_own == 0) return PFAC_OK;
@@ -212,6 +233,7 @@ int pfac_match_packed_async(const pfac_automaton *a, const uint32_t *d_packed, u
 
 int pfac_match_barriers_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv,
                               uint64_t n_own, uint64_t n_avail, int32_t *d_out, void *stream) {
+    DeviceGuard guard;
     if (!a) return fail(PFAC_E_ARG, "pfac_match_barriers_async: null automaton");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_barriers_async: n_avail < n_own");
     if (n_own == 0) return PFAC_OK;
@@ -227,20 +249,20 @@ int pfac_match_barriers_async(const pfac_automaton *a, const uint32_t *d_packed,
     return e ? cuda_fail(e, "pfac_match_barriers_async") : PFAC_OK;
 }
 
-int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out, uint64_t *first_bad,
-               void *stream) {
-    if (!a) return fail(PFAC_E_ARG, "pfac_match: null automaton");
+int pfac_match_checked(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out, uint64_t *first_bad,
+                       void *stream) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_match_checked: null automaton");
     if (first_bad) *first_bad = ~0ull;
     if (n == 0) return PFAC_OK;
-    if (!d_text || !d_out) return fail(PFAC_E_ARG, "pfac_match: null buffer");
-    if (!aligned16(d_out)) return fail(PFAC_E_ARG, "pfac_match: d_out must be 16-byte aligned");
+    if (!d_text || !d_out) return fail(PFAC_E_ARG, "pfac_match_checked: null buffer");
+    if (!aligned16(d_out)) return fail(PFAC_E_ARG, "pfac_match_checked: d_out must be 16-byte aligned");
     const int dev = device_of(d_out);
-    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match: d_out is not device memory");
+    if (dev < 0) return fail(PFAC_E_ARG, "pfac_match_checked: d_out is not device memory");
     cudaStream_t st = (cudaStream_t)stream;
     const uint64_t words = pfac_packed_words(n), iw = pfac_inv_words(n);
     void *scratch = nullptr;
     cudaError_t e = cudaMallocAsync(&scratch, words * 4 + iw * 2 + 16, st);
-    if (e != cudaSuccess) return cuda_fail(e, "pfac_match: scratch allocation");
+    if (e != cudaSuccess) return cuda_fail(e, "pfac_match_checked: scratch allocation");
     uint32_t *d_packed = reinterpret_cast<uint32_t *>(scratch);
     uint16_t *d_inv = reinterpret_cast<uint16_t *>(d_packed + words);
     uint64_t *d_bad = reinterpret_cast<uint64_t *>(d_inv + iw);
@@ -253,15 +275,61 @@ int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32
     if (!rc && !ce) {
         if (first_bad) *first_bad = bad;
         if (bad != ~0ull && !im->K2) {  // barrier semantics live on the filter path
-            rc = fail(PFAC_E_NON_ACGT, "pfac_match: non-ACGT text needs the filter image (PFAC_FB16=1)");
+            rc = fail(PFAC_E_NON_ACGT, "pfac_match_checked: non-ACGT text needs the filter image (PFAC_FB16=1)");
         } else {
             ce = launch_match(*im, d_packed, bad != ~0ull ? d_inv : nullptr, n, n, d_out, stream);
             if (!ce) ce = cudaStreamSynchronize(st);
         }
     }
     cudaFreeAsync(scratch, st);
-    if (ce) return cuda_fail(ce, "pfac_match");
+    if (ce) return cuda_fail(ce, "pfac_match_checked");
     return rc;
+}
+
+int pfac_match(const pfac_automaton *a, const uint8_t *d_text, uint64_t n, int32_t *d_out, void *stream) {
+    return pfac_match_checked(a, d_text, n, d_out, nullptr, stream);
+}
+
+int pfac_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t *first_bad, void *stream) {
+    DeviceGuard guard;
+    if (first_bad) *first_bad = ~0ull;
+    if (n == 0) return PFAC_OK;
+    if (!d_packed || !d_text) return fail(PFAC_E_ARG, "pfac_pack: null buffer");
+    if (!aligned16(d_packed)) return fail(PFAC_E_ARG, "pfac_pack: d_packed must be 16-byte aligned");
+    if (device_of(d_packed) < 0) return fail(PFAC_E_ARG, "pfac_pack: d_packed is not device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t *d_bad = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&d_bad), 8, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pfac_pack: scratch allocation");
+    uint64_t bad = ~0ull;
+    int ce = launch_pack(d_text, n, d_packed, pfac_packed_words(n), d_bad, nullptr, stream);
+    if (!ce) ce = cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d_bad, st);
+    if (!ce) ce = cudaStreamSynchronize(st);
+    if (ce) return cuda_fail(ce, "pfac_pack");
+    if (first_bad) *first_bad = bad;
+    if (bad != ~0ull) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "pfac_pack: byte %llu is not ACGTacgt", (unsigned long long)bad);
+        return fail(PFAC_E_NON_ACGT, msg);
+    }
+    return PFAC_OK;
+}
+
+int pfac_match_packed(const pfac_automaton *a, const uint32_t *d_packed, uint64_t n_own, uint64_t n_avail,
+                      int32_t *d_out, void *stream) {
+    DeviceGuard guard;
+    int rc = pfac_match_packed_async(a, d_packed, n_own, n_avail, d_out, stream);
+    if (rc != PFAC_OK || n_own == 0) return rc;
+    const cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    return e ? cuda_fail(e, "pfac_match_packed") : PFAC_OK;
+}
+
+int pfac_set_text_kernel(pfac_automaton *a, int mode) {
+    if (!a) return fail(PFAC_E_ARG, "pfac_set_text_kernel: null automaton");
+    if (mode < -1 || mode > 2) return fail(PFAC_E_ARG, "pfac_set_text_kernel: mode must be -1, 0, 1 or 2");
+    a->text_kernel.store(mode, std::memory_order_relaxed);
+    return PFAC_OK;
 }
 
 uint64_t pfac_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
@@ -270,6 +338,7 @@ int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d
                                       uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base,
                                       uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity, uint64_t *d_count,
                                       uint64_t *d_hist, void *d_workspace, void *stream) {
+    DeviceGuard guard;
     if (d_inv && !aligned16(d_inv)) return fail(PFAC_E_ARG, "pfac_match_compact_barriers_async: misaligned d_inv");
     if (!a) return fail(PFAC_E_ARG, "pfac_match_compact_async: null automaton");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_compact_async: n_avail < n_own");
@@ -296,6 +365,7 @@ uint64_t pfac_match_list_workspace_bytes(uint64_t n_own) { return compact_worksp
 int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv, uint64_t n_own,
                           uint64_t n_avail, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
                           uint64_t *d_count, uint64_t *d_hist, void *d_workspace, void *stream) {
+    DeviceGuard guard;
     if (!a) return fail(PFAC_E_ARG, "pfac_match_list_async: null automaton");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_list_async: n_avail < n_own");
     if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_match_list_async: null d_count / d_workspace");
@@ -325,15 +395,14 @@ static uint64_t al16(uint64_t x) { return (x + 15) & ~15ull; }
 
 // Which path pfac_match_text_async runs for this image: 0 = pack -> fused kernel, 1 = the text kernel,
 // 2 = the text kernel with 1024-position slices.  The plan's measured preference (MatchPlan::txt_pref,
-// txt1k_pref), overridden by PFAC_TEXT_KERNEL=0 (never) / 1 (whenever one fits; 2048 slices first) /
-// 2 (1024 slices whenever they fit).
-static int text_kernel_for(const DeviceImage &im) {
-    const char *e = getenv("PFAC_TEXT_KERNEL");  // read per call (tests switch it)
-    const int env = e && *e ? atoi(e) : -1;
+// txt1k_pref), unless pfac_set_text_kernel forced 0 (never) / 1 (whenever one fits; 2048 slices
+// first) / 2 (1024 slices whenever they fit).
+static int text_kernel_for(const pfac_automaton *a, const DeviceImage &im) {
+    const int force = a->text_kernel.load(std::memory_order_relaxed);
     const MatchPlan &pl = im.plan;
-    if (!im.K2 || env == 0) return 0;
-    if (env == 2) return pl.txt1k_ok ? 2 : 0;
-    if (env == 1) return pl.txt_ok ? 1 : pl.txt1k_ok ? 2 : 0;
+    if (!im.K2 || force == 0) return 0;
+    if (force == 2) return pl.txt1k_ok ? 2 : 0;
+    if (force == 1) return pl.txt_ok ? 1 : pl.txt1k_ok ? 2 : 0;
     return pl.txt_pref ? 1 : pl.txt1k_pref ? 2 : 0;
 }
 
@@ -352,6 +421,7 @@ int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64
                           int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
                           uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad, void *d_workspace,
                           void *stream) {
+    DeviceGuard guard;
     if (!a) return fail(PFAC_E_ARG, "pfac_match_text_async: null automaton");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_match_text_async: n_avail < n_own");
     if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_match_text_async: null d_count / d_workspace");
@@ -389,7 +459,7 @@ static int match_text_impl(const pfac_automaton *a, DeviceImage &imr, const uint
     int32_t *out = list_only ? reinterpret_cast<int32_t *>(after) : d_out;
     if (list_only) after += al16(n_own * 4);
     int e;
-    const int tk = text_kernel_for(*im);
+    const int tk = text_kernel_for(a, *im);
     if (tk && aligned16(d_text)) {
         e = launch_match_compact(*im, a->k, nullptr, nullptr, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
                                  d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad, nullptr,
@@ -419,6 +489,7 @@ int pfac_match_compact_async(const pfac_automaton *a, const uint32_t *d_packed, 
 int pfac_compact_async(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                        uint64_t capacity, uint64_t *d_count, uint32_t k, uint64_t *d_hist, void *d_workspace,
                        void *stream) {
+    DeviceGuard guard;
     if (!d_count || !d_workspace) return fail(PFAC_E_ARG, "pfac_compact_async: null d_count / d_workspace");
     if (n > 0 && !d_out) return fail(PFAC_E_ARG, "pfac_compact_async: null d_out");
     if (capacity > 0 && (!d_pos || !d_pid)) return fail(PFAC_E_ARG, "pfac_compact_async: null d_pos / d_pid");
@@ -430,6 +501,7 @@ int pfac_compact_async(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint
 
 int pfac_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                  uint64_t capacity, uint64_t *count, uint32_t k, uint64_t *d_hist, void *stream) {
+    DeviceGuard guard;
     if (!count) return fail(PFAC_E_ARG, "pfac_compact: null count");
     if (n > 0 && !d_out) return fail(PFAC_E_ARG, "pfac_compact: null d_out");
     const void *probe = n > 0 ? (const void *)d_out : (const void *)d_pos;
@@ -466,10 +538,9 @@ namespace pfac {
 // Device buffers of one pipeline slot of pfac_scan_host.
 struct ScanSlot {
     uint8_t *text = nullptr;
-    int32_t *out = nullptr;
     uint64_t *pos = nullptr, *cnt = nullptr, *bad = nullptr;
     uint32_t *pid = nullptr;
-    void *ws = nullptr;  // pfac_match_text_workspace_bytes(chunk, chunk + halo, 0)
+    void *ws = nullptr;  // pfac_match_text_workspace_bytes(chunk, chunk + halo, 1): list only, no dense out[]
     uint64_t cap = 0;
     cudaEvent_t h2d = nullptr, done = nullptr;
 };
@@ -483,7 +554,6 @@ struct ScanCtx {
     ~ScanCtx() {
         for (ScanSlot &sl : slot) {
             cudaFree(sl.text);
-            cudaFree(sl.out);
             cudaFree(sl.pos);
             cudaFree(sl.pid);
             cudaFree(sl.cnt);
@@ -505,11 +575,10 @@ struct ScanCtx {
             ScanSlot &sl = slot[i];
             sl.cap = chunk / 8 + 65536;
             e = cudaMalloc(&sl.text, chunk + halo + 16);
-            if (e == cudaSuccess) e = cudaMalloc(&sl.out, chunk * 4 + 16);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
             if (e == cudaSuccess) e = cudaMalloc(&sl.cnt, 16);
-            if (e == cudaSuccess) e = cudaMalloc(&sl.ws, pfac_match_text_workspace_bytes(chunk, chunk + halo, 0));
+            if (e == cudaSuccess) e = cudaMalloc(&sl.ws, pfac_match_text_workspace_bytes(chunk, chunk + halo, 1));
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
             sl.bad = sl.cnt + 1;
@@ -526,6 +595,7 @@ extern "C" {
 int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, uint64_t n_own, uint64_t n_avail,
                    uint64_t pos_base, uint64_t *h_pos, uint32_t *h_pid, uint64_t capacity, uint64_t *count,
                    uint64_t *first_bad) {
+    DeviceGuard guard;
     if (!a || !count) return fail(PFAC_E_ARG, "pfac_scan_host: null automaton / count");
     if (n_avail < n_own) return fail(PFAC_E_ARG, "pfac_scan_host: n_avail < n_own");
     const uint64_t n = n_own, N = n_avail;  // positions to match; bases readable
@@ -560,18 +630,23 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
     uint64_t *h_cnt = X.h_cnt;
     cudaError_t e = cudaSuccess;
     uint64_t total = 0, bad_at = ~0ull;
-    // enqueue chunk c (copy in, the text call -- pack + match + compact in one kernel where the plan
-    // takes it; barriers handled per slice --, count + first owned bad index back to pinned memory)
+    // chunk c owns positions [c*chunk, c*chunk + own) and reads bases up to avail past its start
+    auto own_of = [&](uint64_t c) { return (n - c * chunk) < chunk ? (n - c * chunk) : chunk; };
+    auto avail_of = [&](uint64_t c) {
+        const uint64_t own = own_of(c);
+        return (N - c * chunk) < own + halo ? (N - c * chunk) : own + halo;
+    };
+    // enqueue chunk c (copy in, the text call in list-only form -- pack + match + compact in one kernel
+    // where the plan takes it; barriers handled per slice --, count + first owned bad index back)
     auto enqueue = [&](uint64_t c) -> cudaError_t {
         ScanSlot &sl = slot[c & 1];
-        const uint64_t s0 = c * chunk, own = (n - s0) < chunk ? (n - s0) : chunk;
-        const uint64_t avail = (N - s0) < own + halo ? (N - s0) : own + halo;
+        const uint64_t s0 = c * chunk, own = own_of(c), avail = avail_of(c);
         cudaError_t r = cudaStreamWaitEvent(xs, sl.done, 0);  // the slot's previous chunk is finished
         if (r == cudaSuccess) r = cudaMemcpyAsync(sl.text, h_text + s0, avail, cudaMemcpyHostToDevice, xs);
         if (r == cudaSuccess) r = cudaEventRecord(sl.h2d, xs);
         if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, sl.h2d, 0);
         if (r == cudaSuccess)
-            r = (cudaError_t)match_text_impl(a, *im, sl.text, own, avail, sl.out, pos_base + s0, sl.pos, sl.pid,
+            r = (cudaError_t)match_text_impl(a, *im, sl.text, own, avail, nullptr, pos_base + s0, sl.pos, sl.pid,
                                              sl.cap, sl.cnt, nullptr, sl.bad, sl.ws, cs);
         if (r == cudaSuccess) r = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 16, cudaMemcpyDeviceToHost, cs);
         if (r == cudaSuccess) r = cudaEventRecord(sl.done, cs);
@@ -589,8 +664,7 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
         if (b != ~0ull && bad_at == ~0ull) bad_at = b - pos_base;
         // Dense chunk: grow this slot's list (kept for later calls) and redo it, after the next
         // chunk's enqueue (which touches only the other slot).
-        const uint64_t own = c * chunk + chunk <= n ? chunk : n - c * chunk;
-        const uint64_t avail = (N - c * chunk) < chunk + halo ? N - c * chunk : chunk + halo;
+        const uint64_t own = own_of(c), avail = avail_of(c);
         if (m > sl.cap && e == cudaSuccess) {
             e = cudaStreamSynchronize(cs);
             cudaFree(sl.pos);
@@ -599,7 +673,7 @@ int pfac_scan_host(const pfac_automaton *a, int device, const uint8_t *h_text, u
             if (e == cudaSuccess) e = cudaMalloc(&sl.pos, sl.cap * 8);
             if (e == cudaSuccess) e = cudaMalloc(&sl.pid, sl.cap * 4);
             if (e == cudaSuccess)
-                e = (cudaError_t)match_text_impl(a, *im, sl.text, own, avail, sl.out, pos_base + c * chunk, sl.pos,
+                e = (cudaError_t)match_text_impl(a, *im, sl.text, own, avail, nullptr, pos_base + c * chunk, sl.pos,
                                                  sl.pid, sl.cap, sl.cnt, nullptr, sl.bad, sl.ws, cs);
             if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt + 2 * (c & 1), sl.cnt, 8, cudaMemcpyDeviceToHost, cs);
             if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
@@ -635,6 +709,7 @@ uint64_t pfac_expand_workspace_bytes(void) { return expand_workspace_bytes(); }
 int pfac_expand_async(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *d_pid, const uint64_t *d_count,
                       uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all, uint64_t capacity,
                       uint64_t *d_count_all, void *d_workspace, void *stream) {
+    DeviceGuard guard;
     if (!a) return fail(PFAC_E_ARG, "pfac_expand_async: null automaton");
     if (!d_count || !d_count_all || !d_workspace)
         return fail(PFAC_E_ARG, "pfac_expand_async: null d_count / d_count_all / d_workspace");
@@ -653,6 +728,7 @@ int pfac_expand_async(const pfac_automaton *a, const uint64_t *d_pos, const uint
 
 int pfac_expand(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *d_pid, uint64_t count,
                 uint64_t *d_pos_all, uint32_t *d_pid_all, uint64_t capacity, uint64_t *count_all, void *stream) {
+    DeviceGuard guard;
     if (!count_all) return fail(PFAC_E_ARG, "pfac_expand: null count_all");
     *count_all = 0;
     if (!a) return fail(PFAC_E_ARG, "pfac_expand: null automaton");
@@ -690,6 +766,7 @@ int pfac_expand(const pfac_automaton *a, const uint64_t *d_pos, const uint32_t *
 }
 
 int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out) {
+    DeviceGuard guard;
     if (!a || !out) return fail(PFAC_E_ARG, "pfac_image_info: null argument");
     DeviceImage *im = nullptr;
     int rc = get_image(a, device, &im);
@@ -705,8 +782,11 @@ int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out)
     out->short_pat = im->short_pat;
     out->smem_bytes = im->plan.smem;
     out->l2_persist_bytes = im->l2_persist_bytes;
-    out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4 + h.FB.size() * 4;
-    out->text_kernel = (uint32_t)text_kernel_for(*im);
+    out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4 + h.FB.size() * 4 + h.HR.size() * 4 +
+                       a->prefix_dev.size() * 4 + a->prefix_flat.size() * 4;
+    out->hr_rows = (uint32_t)(h.HR.size() / 4);
+    out->reserved = 0;
+    out->text_kernel = (uint32_t)text_kernel_for(a, *im);
     out->text_window_rows = out->text_kernel == 2 ? im->plan.window_txt1k : im->plan.window_txt;
     return PFAC_OK;
 }

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kCT) compact_kernel(const CompactArgs a) {
     const uint64_t stg = a.stg, pos_base = a.pos_base;
 
     // pass 1: count + stage in order
-    const uint64_t local = warp_stream(a, lo, hi, 0, [&](uint64_t r, uint64_t i, uint32_t val) {
+    const uint64_t local = warp_stream<true>(a, lo, hi, 0, [&](uint64_t r, uint64_t i, uint32_t val) {
         if (r < stg) {
             spos[r] = pos_base + i;
             spid[r] = val;
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kCT) compact_kernel(const CompactArgs a) {
     if (local <= stg) {
         for (uint64_t i = lane; i < local; i += 32) put(prefix + i, spos[i], spid[i]);
     } else {
-        warp_stream(a, lo, hi, prefix, [&](uint64_t r, uint64_t i, uint32_t val) { put(r, pos_base + i, val); });
+        warp_stream<true>(a, lo, hi, prefix, [&](uint64_t r, uint64_t i, uint32_t val) { put(r, pos_base + i, val); });
     }
 }
 

@@ -29,16 +29,19 @@ struct CompactArgs {
     uint32_t *bitmap;     // fused kernel: match bitmaps of the slices its staging could not hold
 };
 
+// NC: out[] was written by an earlier launch (read-only here: ld.global.nc); otherwise (the fused
+// kernels' spill path re-reading cells written in this launch) coherent L2 loads.
+template <bool NC>
 __device__ __forceinline__ void load_step(const int32_t *out, uint64_t n, uint64_t b, uint32_t lane, uint4 (&v)[4]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint64_t idx = b + (uint64_t)(32 * q + lane) * 4;
         if (idx + 4 <= n) {
-            v[q] = ld_stream_v4(out + idx);
+            v[q] = NC ? ld_stream_v4(out + idx) : ld_cg_v4(out + idx);
         } else {
-            v[q].x = idx + 0 < n ? (uint32_t)out[idx + 0] : 0u;
-            v[q].y = idx + 1 < n ? (uint32_t)out[idx + 1] : 0u;
-            v[q].z = idx + 2 < n ? (uint32_t)out[idx + 2] : 0u;
+            v[q].x = idx + 0 < n ? (NC ? (uint32_t)out[idx + 0] : ld_cg_u32(out + idx + 0)) : 0u;
+            v[q].y = idx + 1 < n ? (NC ? (uint32_t)out[idx + 1] : ld_cg_u32(out + idx + 1)) : 0u;
+            v[q].z = idx + 2 < n ? (NC ? (uint32_t)out[idx + 2] : ld_cg_u32(out + idx + 2)) : 0u;
             v[q].w = 0;
         }
     }
@@ -48,15 +51,15 @@ __device__ __forceinline__ void load_step(const int32_t *out, uint64_t n, uint64
 // position order, rank counted from wbase.  Returns the number of nonzero entries.
 // bits (nullable): a position-indexed bitmap (bit i%32 of word i/32); when given, only entries whose
 // bit is set count (the list-only kernel's out[] scratch holds values only there).  lo is a multiple of 32.
-template <typename Emit>
+template <bool NC, typename Emit>
 __device__ __forceinline__ uint64_t warp_stream(const CompactArgs &a, uint64_t lo, uint64_t hi, uint64_t wbase,
                                                 Emit emit, const uint32_t *bits = nullptr) {
     const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1;
     uint64_t local = 0;
     uint4 v[4], vn[4];
-    if (lo < hi) load_step(a.out, a.n, lo, lane, v);
+    if (lo < hi) load_step<NC>(a.out, a.n, lo, lane, v);
     for (uint64_t b = lo; b < hi; b += kStep) {
-        if (b + kStep < hi) load_step(a.out, a.n, b + kStep, lane, vn);
+        if (b + kStep < hi) load_step<NC>(a.out, a.n, b + kStep, lane, vn);
         if (bits) {  // lane's 4 positions b + 128q + 4 lane .. +3: a nibble of word (b + 128q)/32 + lane/8
 #pragma unroll
             for (int q = 0; q < 4; ++q) {

@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             const uint64_t spill_first = s_first + spill_rel;
             const uint64_t lo = spill_first * kSliceT < p.n_own ? spill_first * kSliceT : p.n_own;
             const uint64_t hi = s_end * kSliceT < p.n_own ? s_end * kSliceT : p.n_own;
-            warp_stream(
+            warp_stream<false>(
                 p.c, lo, hi, prefix + wstaged,
                 [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); },
                 LIST ? p.c.bitmap : nullptr);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <array>
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -130,6 +131,7 @@ struct pfac_automaton {
     std::vector<uint32_t> prefix_dev;  // 4*(k+1): (chain length, parent, flat base lo, hi) per pattern
     std::vector<uint32_t> prefix_flat; // every pattern's chain, shortest first, at its flat base
     pfac::HostImage host_image;   // derived once at build
+    std::atomic<int> text_kernel{-1};  // pfac_set_text_kernel: -1 = the plan's choice, else forced 0/1/2
     std::mutex mu;                // guards images
     std::vector<pfac::DeviceImage *> images;
 };

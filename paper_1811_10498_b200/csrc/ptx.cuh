@@ -60,6 +60,16 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void *p) {
                  : "l"(p));
     return r;
 }
+// L2-only 16-byte load: coherent with stores made earlier in the same launch (the fused kernels'
+// spill path re-reads out[] cells this launch wrote; .nc would be undefined there)
+__device__ __forceinline__ uint4 ld_cg_v4(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
 __device__ __forceinline__ uint32_t ld_cg_u32(const int32_t *p) {  // L2 only: sees this warp's stores
     uint32_t v;
     asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

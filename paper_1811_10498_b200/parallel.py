@@ -128,3 +128,74 @@ def unpack_lists(gathered, cap: int):
     pos = [g[r, 8:8 + 8 * cap].contiguous().view(torch.int64)[:c] for r, c in enumerate(counts)]
     pid = [g[r, 8 + 8 * cap:8 + 12 * cap].contiguous().view(torch.int32)[:c] for r, c in enumerate(counts)]
     return torch.cat(pos), torch.cat(pid), counts
+
+
+# ----------------------------------------------------------------------------- one rank's step
+class ShardedMatcher:
+    """One rank's part of the N-GPU hot path.
+
+    The rank holds its text shard (owned positions + a (maxlen - 1)-base halo, `Shard`) on its GPU.
+    A step is the text call -- pack + match + compact in one kernel (pfac_match_text_async) -- with
+    pos_base = s_g, writing the count and the (position, pattern id) list straight into the rank's
+    list buffer, followed (N > 1) by one gather of the fixed-size buffers to `dst`.  No text moves
+    between GPUs; the only collective is the gather (rank order = position order).
+
+    cap: list capacity, the same on every rank (see `agree_capacity`).  dense_out: also write the
+    dense out[] of the owned positions (the paper's output array).
+    """
+
+    def __init__(self, a, d_text, sh: Shard, cap: int, dense_out: bool = True, group=None, dst: int = 0):
+        import torch
+
+        from . import binding as B
+        self.a, self.d_text, self.sh, self.cap, self.group, self.dst = a, d_text, sh, cap, group, dst
+        dev = d_text.device
+        self.buf, self.count, self.pos, self.pid = list_buffer(cap, dev)
+        self.out = torch.empty(max(sh.n_own, 1), dtype=torch.int32, device=dev)[:sh.n_own] if dense_out else None
+        self.ws = torch.empty(B.match_text_workspace_bytes(sh.n_own, sh.n_avail, not dense_out), dtype=torch.uint8,
+                              device=dev)
+        self.first_bad = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def match(self, stream=None) -> None:
+        """The rank's text call (asynchronous on `stream`)."""
+        from . import binding as B
+        B.match_text_async(self.a, self.d_text, self.sh.n_own, self.sh.n_avail, self.out, self.pos, self.pid,
+                           self.count, self.ws, pos_base=self.sh.start, first_bad=self.first_bad, stream=stream)
+
+    def gather(self):
+        """gather_lists_async of this rank's buffer: (world, nbytes) on dst, None elsewhere."""
+        return gather_lists_async(self.buf, group=self.group, dst=self.dst)
+
+    def step(self, stream=None):
+        self.match(stream)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            return self.gather()
+        return None
+
+
+def probe_count(a, d_text, sh: Shard) -> int:
+    """The exact match count of this rank's shard (a capacity-0 text call; synchronous)."""
+    import torch
+
+    from . import binding as B
+    dev = d_text.device
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    empty64 = torch.empty(1, dtype=torch.int64, device=dev)[:0]
+    empty32 = torch.empty(1, dtype=torch.int32, device=dev)[:0]
+    ws = torch.empty(B.match_text_workspace_bytes(sh.n_own, sh.n_avail, True), dtype=torch.uint8, device=dev)
+    B.match_text_async(a, d_text, sh.n_own, sh.n_avail, None, empty64, empty32, cnt, ws, pos_base=sh.start)
+    return int(cnt.item())
+
+
+def agree_capacity(local_count: int, group=None, slack: int = 1024) -> int:
+    """One list capacity for every rank: the largest rank's count + slack (all_reduce MAX; outside
+    the timed region).  gloo reduces on the host, NCCL on the device."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local_count + slack
+    dev = "cpu" if dist.get_backend(group) == "gloo" else torch.device("cuda", torch.cuda.current_device())
+    t = torch.tensor([local_count + slack], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())

@@ -281,26 +281,20 @@ def _full_config(idx):
     del packed, ws
     # the text-input call (pack fused into the kernel; the bench default where the plan takes it) in
     # both of its paths, on the same full input: list, count, first_bad and the whole dense out[]
-    prev = os.environ.get("PFAC_TEXT_KERNEL")
-    try:
-        for mode in ("1", "0", "2"):
-            os.environ["PFAC_TEXT_KERNEL"] = mode
-            ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
-            out3 = torch.empty(n, dtype=torch.int32, device=DEV)
-            bad = torch.zeros(1, dtype=torch.int64, device=DEV)
-            pos2.fill_(-1)
-            P.match_text_async(a, dtext, n, n, out3, pos2, pid2, cnt, ws, first_bad=bad)
-            torch.cuda.synchronize()
-            assert int(cnt.item()) == len(epos) and int(bad.item()) == -1
-            assert (pos2[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
-            assert (pid2[:len(epos)].cpu().numpy() == epid).all()
-            assert bool((out3 == out).all())
-            del out3, ws
-    finally:
-        if prev is None:
-            os.environ.pop("PFAC_TEXT_KERNEL", None)
-        else:
-            os.environ["PFAC_TEXT_KERNEL"] = prev
+    for mode in (1, 0, 2):
+        a.set_text_kernel(mode)
+        ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
+        out3 = torch.empty(n, dtype=torch.int32, device=DEV)
+        bad = torch.zeros(1, dtype=torch.int64, device=DEV)
+        pos2.fill_(-1)
+        P.match_text_async(a, dtext, n, n, out3, pos2, pid2, cnt, ws, first_bad=bad)
+        torch.cuda.synchronize()
+        assert int(cnt.item()) == len(epos) and int(bad.item()) == -1
+        assert (pos2[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
+        assert (pid2[:len(epos)].cpu().numpy() == epid).all()
+        assert bool((out3 == out).all())
+        del out3, ws
+    a.set_text_kernel(-1)
     # sampled out[] windows (every element, including the zeros)
     o = Oracle(pats)
     n = len(text)
@@ -457,30 +451,24 @@ def test_config2_fasta_full_text_kernel():
     epos, epid = _oracle_list_parallel(pats, text)
     bad_idx = int(np.nonzero(~np.isin(text[:1000], np.frombuffer(b"ACGTacgt", np.uint8)))[0][0])
     o = Oracle(pats)
-    prev = os.environ.get("PFAC_TEXT_KERNEL")
-    try:
-        for mode in ("1", "0"):
-            os.environ["PFAC_TEXT_KERNEL"] = mode
-            out = torch.empty(n, dtype=torch.int32, device=DEV)
-            cap = len(epos) + 1024
-            pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
-            pid = torch.empty(cap, dtype=torch.int32, device=DEV)
-            cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
-            bad = torch.zeros(1, dtype=torch.int64, device=DEV)
-            ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
-            P.match_text_async(a, dtext, n, n, out, pos, pid, cnt, ws, first_bad=bad)
-            torch.cuda.synchronize()
-            assert int(cnt.item()) == len(epos) and int(bad.item()) == bad_idx
-            assert (pos[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
-            assert (pid[:len(epos)].cpu().numpy() == epid).all()
-            for s in [0, n // 2 + 3, n - 90_001]:
-                assert (out[s:s + 90_000].cpu().numpy() == o.match(text, s, s + 90_000)).all()
-            del out, ws
-    finally:
-        if prev is None:
-            os.environ.pop("PFAC_TEXT_KERNEL", None)
-        else:
-            os.environ["PFAC_TEXT_KERNEL"] = prev
+    for mode in (1, 0):
+        a.set_text_kernel(mode)
+        out = torch.empty(n, dtype=torch.int32, device=DEV)
+        cap = len(epos) + 1024
+        pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
+        pid = torch.empty(cap, dtype=torch.int32, device=DEV)
+        cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+        bad = torch.zeros(1, dtype=torch.int64, device=DEV)
+        ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
+        P.match_text_async(a, dtext, n, n, out, pos, pid, cnt, ws, first_bad=bad)
+        torch.cuda.synchronize()
+        assert int(cnt.item()) == len(epos) and int(bad.item()) == bad_idx
+        assert (pos[:len(epos)].cpu().numpy() == epos.astype(np.int64)).all()
+        assert (pid[:len(epos)].cpu().numpy() == epid).all()
+        for s in [0, n // 2 + 3, n - 90_001]:
+            assert (out[s:s + 90_000].cpu().numpy() == o.match(text, s, s + 90_000)).all()
+        del out, ws
+    a.set_text_kernel(-1)
 
 
 @pytest.mark.skipif(bool(os.environ.get("PFAC_SKIP_FULL")), reason="PFAC_SKIP_FULL set (4.3 Gbase run)")
@@ -496,26 +484,20 @@ def test_text_beyond_2pow32_positions():
     epos, epid = _oracle_list_parallel(pats, text)
     assert len(epos) > 1_000_000 and int(epos[-1]) > (1 << 32)
     o = Oracle(pats)
-    prev = os.environ.get("PFAC_TEXT_KERNEL")
-    try:
-        for mode in ("1", "0"):
-            os.environ["PFAC_TEXT_KERNEL"] = mode
-            out = torch.empty(n, dtype=torch.int32, device=DEV)
-            cap = len(epos) + 1024
-            pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
-            pid = torch.empty(cap, dtype=torch.int32, device=DEV)
-            cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
-            ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
-            P.match_text_async(a, dtext, n, n, out, pos, pid, cnt, ws, pos_base=3)
-            torch.cuda.synchronize()
-            assert int(cnt.item()) == len(epos)
-            assert (pos[:len(epos)].cpu().numpy() == epos.astype(np.int64) + 3).all()
-            assert (pid[:len(epos)].cpu().numpy() == epid).all()
-            for s in [(1 << 32) - 50_000, n - 60_001]:
-                assert (out[s:s + 60_000].cpu().numpy() == o.match(text, s, s + 60_000)).all()
-            del out, ws
-    finally:
-        if prev is None:
-            os.environ.pop("PFAC_TEXT_KERNEL", None)
-        else:
-            os.environ["PFAC_TEXT_KERNEL"] = prev
+    for mode in (1, 0):
+        a.set_text_kernel(mode)
+        out = torch.empty(n, dtype=torch.int32, device=DEV)
+        cap = len(epos) + 1024
+        pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
+        pid = torch.empty(cap, dtype=torch.int32, device=DEV)
+        cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+        ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
+        P.match_text_async(a, dtext, n, n, out, pos, pid, cnt, ws, pos_base=3)
+        torch.cuda.synchronize()
+        assert int(cnt.item()) == len(epos)
+        assert (pos[:len(epos)].cpu().numpy() == epos.astype(np.int64) + 3).all()
+        assert (pid[:len(epos)].cpu().numpy() == epid).all()
+        for s in [(1 << 32) - 50_000, n - 60_001]:
+            assert (out[s:s + 60_000].cpu().numpy() == o.match(text, s, s + 60_000)).all()
+        del out, ws
+    a.set_text_kernel(-1)

@@ -1,0 +1,45 @@
+"""compute-sanitizer over every libpfac kernel instantiation (-m gpu, slow): memcheck (out-of-bounds
+and misaligned accesses, including the TMA bulk copies' global sources), racecheck (shared-memory
+hazards between the per-warp slice buffers, the mbarrier-guarded TMA refills and the staging
+areas), synccheck (illegal __syncwarp / barrier use) and initcheck (reads of uninitialised device
+memory: the workspaces are documented as "any content").  The workload (tests/sanitize_workload.py)
+also checks every result against the oracle, so a tool run that changes timing still has to be
+correct.  A run passes when the tool reports 0 errors and the workload exits 0; the summary lines
+are appended to gpurun_out/sanitizer.log when that directory exists (profiles/ keeps the copy)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not found")
+    env = dict(os.environ, PFAC_SANITIZE_N="70001" if tool == "memcheck" else "20001")
+    extra = ["--racecheck-report", "all"] if tool == "racecheck" else []
+    cmd = [SAN, "--tool", tool, *extra, "--error-exitcode", "99", "--print-limit", "20",
+           sys.executable, os.path.join(ROOT, "tests", "sanitize_workload.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    summary = [ln for ln in out.splitlines() if "ERROR SUMMARY" in ln or "RACECHECK SUMMARY" in ln]
+    log_dir = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(log_dir):
+        with open(os.path.join(log_dir, "sanitizer.log"), "a") as f:
+            f.write(f"### {tool} (rc {r.returncode})\n" + "\n".join(summary) + "\n")
+            if r.returncode != 0:
+                f.write(out[-6000:] + "\n")
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize_workload ok" in out
+    assert any("0 errors" in s or "0 hazards" in s for s in summary), summary

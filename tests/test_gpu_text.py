@@ -32,7 +32,7 @@ def text_kernel(request, monkeypatch):
     """Both paths of pfac_match_text_async: the one-kernel TXT instantiation and the pack + fused
     kernel path the call takes for unaligned text or automata the policy keeps off TXT; "2": the text
     kernel with 1024-position slices (uint32 images; uint16 ones take the two-kernel path)."""
-    monkeypatch.setenv("PFAC_TEXT_KERNEL", request.param)
+    monkeypatch.setattr(P.binding, "DEFAULT_TEXT_KERNEL", int(request.param))
     return request.param
 
 
@@ -183,14 +183,15 @@ def test_text_hist_capacity():
     assert (pos2 == epos[:cap].astype(np.int64)).all() and (pid2 == epid[:cap].astype(np.int32)).all()
 
 
-def test_text_policy_info():
+def test_text_policy_info(text_kernel):
     """The image reports which path the call takes (pfac_image_info.text_kernel)."""
     a = P.Automaton(SETS["cfg2like"]())
     info = a.image_info(0)
-    import os
-    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 0}[os.environ["PFAC_TEXT_KERNEL"]]  # uint16 image
+    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 0}[text_kernel]  # uint16 image
     b = P.Automaton(SETS["big32"]())  # uint32 image
-    assert b.image_info(0)["text_kernel"] == {"1": 1, "0": 0, "2": 2}[os.environ["PFAC_TEXT_KERNEL"]]
+    assert b.image_info(0)["text_kernel"] == {"1": 1, "0": 0, "2": 2}[text_kernel]
+    b.set_text_kernel(-1)  # back to the plan: a uint32 image with < 2^20 rows takes 2048-slice text
+    assert b.image_info(0)["text_kernel"] in (1, 2)
 
 
 def test_text_empty():
