@@ -58,6 +58,34 @@ def profiled_traffic(cfg_idx: int, path: str):
     return None if e is None else float(e["dram_bytes_per_launch"])
 
 
+def secondary_bounds(cfg_idx: int, n: int, kernel_ms: float):
+    """The text kernel's other ceilings (cfg4 min(HBM, L2 random gather), cfg5 issue),
+    from the per-base counts of the committed ncu capture (profiles/ncu_bounds.json) and the measured
+    L2 gather rate (profiles/r01_microbench.json): each floor is the time that resource alone needs at
+    its peak; frac = floor / the measured kernel time."""
+    pb = os.path.join(ROOT, "profiles", "ncu_bounds.json")
+    pm = os.path.join(ROOT, "profiles", "r01_microbench.json")
+    if not (os.path.exists(pb) and os.path.exists(pm)):
+        return None
+    b = json.load(open(pb)).get(f"cfg{cfg_idx}")
+    if not b:
+        return None
+    mb = json.load(open(pm))
+    gather = max(x["gsectors_per_s"] for x in mb["l2_gather_32B"]) * 1e9
+    attrs = mb["device_attrs"]
+    issue = attrs["sms"] * 4 * attrs["sm_clock_khz"] * 1e3  # warp instructions / s (4 schedulers per SM)
+    l2_ms = b["l2_sectors_read_per_base"] * n / gather * 1e3
+    is_ms = b["warp_inst_per_base"] * n / issue * 1e3
+    return {
+        "l2_gather": {"sectors_per_base": b["l2_sectors_read_per_base"], "peak_gsectors_s": gather / 1e9,
+                      "floor_ms": l2_ms, "frac": l2_ms / kernel_ms},
+        "issue": {"warp_inst_per_base": b["warp_inst_per_base"], "peak_ginst_s": issue / 1e9,
+                  "floor_ms": is_ms, "frac": is_ms / kernel_ms,
+                  "simt_threads_per_inst": b.get("threads_per_warp_inst")},
+        "source": f"profiles/ncu_bounds.json ({b.get('report')}), profiles/r01_microbench.json",
+    }
+
+
 class ClockSampler:
     """nvml SM clock + throttle reasons sampled in a thread during the timed region."""
 
@@ -497,9 +525,13 @@ def run_pfac(args):
     elif text_in:  # the call's pack + first-bad + fused kernels: their bytes together
         match_bpb = (PACK_BYTES_PER_BASE + 2 * BARRIER_BYTES_PER_BASE + 0.25 +
                      (12.0 * m_final / max(1, n_own) if list_only else 4.0))
+    if fused and not list_only:  # the dense paths also write the list: 12 B per match (8 pos + 4 id)
+        match_bpb += 12.0 * m_final / max(1, n_own)
     pack_bpb = PACK_BYTES_PER_BASE + (BARRIER_BYTES_PER_BASE if bars else 0.0)
     match_gbs = match_bpb * n_own / (match_ms * 1e-3) / 1e9
     traffic = profiled_traffic(args.config, args.path) if args.n is None and not bars else None
+    other_bounds = secondary_bounds(args.config, n_own, match_ms) if (
+        args.n is None and not bars and text_one and not list_only) else None
 
     # ---- e2e: the same work through the C-ABI's host-memory entry point (pfac_scan_host): the text
     # from pinned HOST memory, chunked H2D overlapped with the kernels, the list copied back to HOST
@@ -576,7 +608,8 @@ def run_pfac(args):
                                     "match_kernel<FUSE=1> (match + compact)" if fused else "match_kernel")
                          + ("<BAR=1>" if bars else ""),
                          "algorithmic_bytes_per_launch": match_bpb * n_own, "peak_source": hbm_src,
-                         "kernel_ms": match_ms, "kernel_ms_source": dominant_src},
+                         "kernel_ms": match_ms, "kernel_ms_source": dominant_src,
+                         **({"other_bounds": other_bounds} if other_bounds else {})},
             "path": args.path + (" (one kernel)" if text_one else " (pack + fused kernel)" if text_in else ""),
             "cuda_graph": graph is not None, **({"cuda_graph_error": graph_error} if graph_error else {}),
             "kernels_ms": {"pack": pack_ms, ("match+compact (fused)" if fused else "match"): match_ms,

@@ -289,7 +289,8 @@ typedef struct {
                                  1 = one kernel, 2 = one kernel with 1024-position slices */
     uint32_t text_window_rows;/* rows staged in shared memory by that kernel */
     uint32_t hr_rows;         /* chain-head row copies next to J2 (uint32 images; 0 = none) */
-    uint32_t reserved;
+    uint32_t hr_nb_rows;      /* of which NOFIN chains whose J2 entry carries their first 4 bases
+                                 (a walk that differs there answers 0 without loading the row) */
 } pfac_image_info_t;
 int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out);
 

@@ -115,7 +115,7 @@ class ImageInfo(ctypes.Structure):
                 ("all_smem", ctypes.c_uint32), ("short_pat", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint64),
                 ("l2_persist_bytes", ctypes.c_uint64), ("image_bytes", ctypes.c_uint64),
                 ("text_kernel", ctypes.c_uint32), ("text_window_rows", ctypes.c_uint32),
-                ("hr_rows", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("hr_rows", ctypes.c_uint32), ("hr_nb_rows", ctypes.c_uint32)]
 
 
 class PfacError(RuntimeError):

@@ -785,7 +785,7 @@ int pfac_image_info(const pfac_automaton *a, int device, pfac_image_info_t *out)
     out->image_bytes = h.J.size() + h.T.size() + h.F.size() + h.J2.size() * 4 + h.FB.size() * 4 + h.HR.size() * 4 +
                        a->prefix_dev.size() * 4 + a->prefix_flat.size() * 4;
     out->hr_rows = (uint32_t)(h.HR.size() / 4);
-    out->reserved = 0;
+    out->hr_nb_rows = h.hr_nb;
     out->text_kernel = (uint32_t)text_kernel_for(a, *im);
     out->text_window_rows = out->text_kernel == 2 ? im->plan.window_txt1k : im->plan.window_txt;
     return PFAC_OK;

@@ -276,7 +276,7 @@ void derive_host_image(pfac_automaton *a) {
     im.rows = ((S + 1) + 7) & ~7u;
     const uint32_t cell = im.cell;
     const uint32_t chain_flag = cell == 2 ? 0x8000u : 0x80000000u;
-    im.T.assign((size_t)im.rows * 4 * cell, 0);
+    im.T.assign((size_t)im.rows * kRowCells * cell, 0);
     im.F.assign((size_t)im.rows * cell, 0);
     auto putc = [&](std::vector<uint8_t> &v, size_t i, uint32_t x) {
         if (cell == 2) put<uint16_t>(v, i, x);
@@ -285,6 +285,7 @@ void derive_host_image(pfac_automaton *a) {
     for (uint32_t u = 0; u < S; ++u) {
         const uint32_t d = dev[u];
         putc(im.F, d, a->F[u]);
+        if (kMergedF) putc(im.T, (size_t)d * kRowCells + 4, a->F[u]);  // ablation: F inside the row
         uint32_t v0;
         if (unary_next(u, v0)) {  // chain row: the next L <= 16 forced bases within u's part
             uint32_t bits = 0, L = 0, v = u, c, w;
@@ -297,18 +298,18 @@ void derive_host_image(pfac_automaton *a) {
                 ++L;
             }
             const uint32_t nofin = inner_final ? 0u : (cell == 2 ? 0x4000u : 0x40000000u);
-            putc(im.T, (size_t)d * 4 + 0, chain_flag | nofin | L);
+            putc(im.T, (size_t)d * kRowCells + 0, chain_flag | nofin | L);
             if (cell == 2) {
-                putc(im.T, (size_t)d * 4 + 1, bits & 0xFFFFu);
-                putc(im.T, (size_t)d * 4 + 2, bits >> 16);
-                putc(im.T, (size_t)d * 4 + 3, a->F[u]);
+                putc(im.T, (size_t)d * kRowCells + 1, bits & 0xFFFFu);
+                putc(im.T, (size_t)d * kRowCells + 2, bits >> 16);
+                putc(im.T, (size_t)d * kRowCells + 3, a->F[u]);
             } else {
-                putc(im.T, (size_t)d * 4 + 1, bits);
-                putc(im.T, (size_t)d * 4 + 2, a->F[u]);
+                putc(im.T, (size_t)d * kRowCells + 1, bits);
+                putc(im.T, (size_t)d * kRowCells + 2, a->F[u]);
             }
         } else {
             for (int c = 0; c < 4; ++c)
-                if (uint32_t v = tab[(size_t)u * 4 + c]) putc(im.T, (size_t)d * 4 + c, dev[v]);
+                if (uint32_t v = tab[(size_t)u * 4 + c]) putc(im.T, (size_t)d * kRowCells + c, dev[v]);
         }
     }
     const uint32_t nk = 1u << (2 * K);
@@ -343,6 +344,7 @@ void derive_host_image(pfac_automaton *a) {
         // L2-persisting window; cell 3 (unused in chain rows) holds the head's device id, and the
         // J2 entry becomes ALIVE | HRF | index.  Branch heads keep pointing into T.
         im.HR.clear();
+        im.hr_nb = 0;
         if (cell == 4 && im.S < (1u << 30)) {
             uint64_t heads = 0;
             for (uint64_t x = 0; x < n2; ++x)
@@ -352,12 +354,21 @@ void derive_host_image(pfac_automaton *a) {
                     if (!(im.J2[x] & 0x80000000u)) continue;
                     const uint32_t s = im.J2[x] & 0x7FFFFFFFu;
                     uint32_t row[4];
-                    memcpy(row, im.T.data() + (size_t)s * 16, 16);
+                    memcpy(row, im.T.data() + (size_t)s * kRowCells * 4, 16);
                     if (!(row[0] & 0x80000000u)) continue;  // a branch row: stays in T
                     row[3] = s;
                     const uint32_t h = (uint32_t)(im.HR.size() / 4);
                     im.HR.insert(im.HR.end(), row, row + 4);
-                    im.J2[x] = 0x80000000u | 0x40000000u | h;
+                    // NB form: a NOFIN chain of L >= 4 forced bases whose head answers 0 (F = 0, so
+                    // every state strictly inside the span answers 0 too).  The entry carries the
+                    // first 4 forced bases; a walk whose next 4 bases differ (or that has fewer than
+                    // 4 left) ends inside the span and answers 0 without loading the row (all but
+                    // ~1/256 of the live walks on random text).
+                    const bool nb = (row[0] & 0x40000000u) && (row[0] & 31u) >= kHRBases && row[2] == 0 &&
+                                    h < (1u << kHRIndexBitsNB);
+                    im.hr_nb += nb ? 1u : 0u;
+                    im.J2[x] = nb ? kJ2Alive | kJ2HR | kJ2NB | ((row[1] & 0xFFu) << kHRIndexBitsNB) | h
+                                  : kJ2Alive | kJ2HR | h;
                 }
             }
         }

@@ -26,7 +26,10 @@ struct CompactArgs {
     uint32_t *stage_pid;
     uint64_t stg;         // staging entries per warp
     uint64_t chunk;       // ints per warp (multiple of kStep)
-    uint32_t *bitmap;     // fused kernel: match bitmaps of the slices its staging could not hold
+    uint32_t *bitmap;     // fused kernel: match bitmaps of the slices its staging and log could not hold
+    uint8_t *log;         // fused kernel: per-warp match logs (log_pw bytes each, 16-byte multiple)
+    uint64_t log_pw;
+    uint32_t pid16;       // log pids as uint16 (every id < 2^16)
 };
 
 // NC: out[] was written by an earlier launch (read-only here: ld.global.nc); otherwise (the fused
@@ -149,6 +152,14 @@ __device__ __forceinline__ void put_match(const CompactArgs &a, uint64_t r, uint
 // Workspace of the fused kernel's spilled slice bitmaps: one bit per position, whole slices
 // (a slice is <= 65536 positions), 16-byte multiple.
 inline uint64_t spill_bitmap_bytes(uint64_t n) { return (((n + 65536) / 32) * 4 + 15) & ~15ull; }
+
+// The fused kernels' per-warp match logs: 1 byte per position (a slice's record -- its match bitmap
+// and the pids of its matches -- costs 8 + n/8 + 2 or 4 bytes per match, so the log holds every
+// slice of a warp's run up to ~43% (uint16 pids) / ~22% (uint32) match density; denser runs spill).
+inline uint64_t match_log_bytes(uint64_t n) { return (n + 15) & ~15ull; }
+__host__ __device__ constexpr uint32_t log_record_bytes(uint32_t bm_words, uint32_t cnt, uint32_t pid_bytes) {
+    return (8 + bm_words * 4 + cnt * pid_bytes + 15) & ~15u;
+}
 
 inline uint64_t stage_entries(uint64_t n) {
     const uint64_t cap = kStageBytes / 12;

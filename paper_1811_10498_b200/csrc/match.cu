@@ -97,6 +97,7 @@ struct Row;
 template <>
 struct Row<uint16_t> {
     uint2 r;
+    uint32_t f;  // PFAC_MERGED_F: F(s) from the row's cell 4
     __device__ __forceinline__ bool chain() const { return r.x & 0x8000u; }
     __device__ __forceinline__ bool nofin() const { return r.x & 0x4000u; }
     __device__ __forceinline__ uint32_t len() const { return r.x & 31u; }
@@ -107,6 +108,7 @@ struct Row<uint16_t> {
 template <>
 struct Row<uint32_t> {
     uint4 r;
+    uint32_t f;  // PFAC_MERGED_F: F(s) from the row's cell 4
     __device__ __forceinline__ bool chain() const { return r.x & 0x80000000u; }
     __device__ __forceinline__ bool nofin() const { return r.x & 0x40000000u; }
     __device__ __forceinline__ uint32_t len() const { return r.x & 31u; }
@@ -117,26 +119,64 @@ struct Row<uint32_t> {
     }
 };
 
+// Table loads (rows, F, J2, HR): read-only for the whole launch, so ld.global.nc (L1-cached) by
+// default; PFAC_TAB_CG=1 is the ablation with ld.global.cg (L2 only) -- the B200 analogue of the
+// paper's -Xptxas -dlcm=cg runs.
+#ifndef PFAC_TAB_CG
+#define PFAC_TAB_CG 0
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_tab(const T *p) {
+#if PFAC_TAB_CG
+    return __ldcg(p);
+#else
+    return __ldg(p);
+#endif
+}
+
 template <typename CT, bool WIN>
 struct Tab {
     const CT *Tw, *Fw, *Tg, *Fg;
     uint32_t W;
     __device__ __forceinline__ Row<CT> row(uint32_t s) const {
         Row<CT> r;
-        if constexpr (sizeof(CT) == 2) {
-            if (!WIN || s < W) r.r = *reinterpret_cast<const uint2 *>(Tw + (size_t)s * 4);
-            else r.r = __ldg(reinterpret_cast<const uint2 *>(Tg + (size_t)s * 4));
+        const size_t b = (size_t)s * kRowCells;
+        if constexpr (sizeof(CT) == 2 && kMergedF) {  // one 16-byte row: 4 transitions, F, padding
+            const uint4 v = (!WIN || s < W) ? *reinterpret_cast<const uint4 *>(Tw + b)
+                                            : ld_tab(reinterpret_cast<const uint4 *>(Tg + b));
+            r.r = make_uint2(v.x, v.y);
+            r.f = v.z & 0xFFFFu;
+        } else if constexpr (sizeof(CT) == 2) {
+            if (!WIN || s < W) r.r = *reinterpret_cast<const uint2 *>(Tw + b);
+            else r.r = ld_tab(reinterpret_cast<const uint2 *>(Tg + b));
         } else {
-            if (!WIN || s < W) r.r = *reinterpret_cast<const uint4 *>(Tw + (size_t)s * 4);
-            else r.r = __ldg(reinterpret_cast<const uint4 *>(Tg + (size_t)s * 4));
+            if (!WIN || s < W) r.r = *reinterpret_cast<const uint4 *>(Tw + b);
+            else r.r = ld_tab(reinterpret_cast<const uint4 *>(Tg + b));
+            if constexpr (kMergedF) r.f = (!WIN || s < W) ? (uint32_t)Tw[b + 4] : (uint32_t)ld_tab(Tg + b + 4);
         }
         return r;
     }
     __device__ __forceinline__ uint32_t final_of(uint32_t s) const {
-        if constexpr (!WIN) return Fw[s];
-        else return s < W ? (uint32_t)Fw[s] : (uint32_t)__ldg(Fg + s);
+        if constexpr (kMergedF) {
+            const size_t b = (size_t)s * kRowCells + 4;
+            if constexpr (!WIN) return Tw[b];
+            else return s < W ? (uint32_t)Tw[b] : (uint32_t)ld_tab(Tg + b);
+        } else if constexpr (!WIN) {
+            return Fw[s];
+        } else {
+            return s < W ? (uint32_t)Fw[s] : (uint32_t)ld_tab(Fg + s);
+        }
     }
 };
+
+// Rank of this lane's first set bit among the warp's 4-bit masks m (lane order), via three ballots
+// of the per-lane counts (0..4); tot = the warp's total.  lt = lanes below this one.
+__device__ __forceinline__ uint32_t nibble_rank(uint32_t m, uint32_t lt, uint32_t &tot) {
+    const uint32_t c = __popc(m);
+    const uint32_t b0 = __ballot_sync(~0u, c & 1), b1 = __ballot_sync(~0u, c & 2), b2 = __ballot_sync(~0u, c & 4);
+    tot = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+    return __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+}
 
 // 16 bases starting at local offset l (base i in bits 2i).
 __device__ __forceinline__ uint32_t window16(const uint32_t *txt, uint32_t l) {
@@ -170,7 +210,10 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
             l += L;
         } else {
             const uint32_t t = r.child(w & 3u);
-            if (!t) break;
+            if (!t) {
+                if constexpr (kMergedF) return r.f;  // the answer came with the row
+                break;
+            }
             s = t;
             ++l;
         }
@@ -223,6 +266,10 @@ constexpr bool kContiguousSchedule = PFAC_CONTIG;
 #endif
 constexpr uint32_t kDrainIPL = PFAC_DRAIN_IPL;  // queued items per lane per drain round (A/B knob)
 constexpr uint32_t kQCap = 32 * kDrainIPL + 64;  // queue of flagged positions
+#ifndef PFAC_PUSH_SCAN
+#define PFAC_PUSH_SCAN 1  // A/B knob: 0 = one ballot round per queued position per lane
+#endif
+constexpr bool kPushScan = PFAC_PUSH_SCAN;
 constexpr int kFBK = kFilterK;                         // filter length K1 (FBM)
 constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared memory (4^10: 128 KiB)
 
@@ -257,8 +304,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     CT *sJ = reinterpret_cast<CT *>(smem);                 // J (4^K cells) ...
     const uint32_t *sFB = reinterpret_cast<const uint32_t *>(smem);  // ... or, FBM: the K1-mer filter
     CT *sT = reinterpret_cast<CT *>(smem + (FBM ? kFBBytes : NJ * sizeof(CT)));
-    CT *sF = sT + (size_t)p.window * 4;
-    uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + p.window);  // 16-byte aligned (W % 8 == 0)
+    CT *sF = sT + (size_t)p.window * kRowCells;
+    uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + (kMergedF ? 0 : p.window));  // 16-byte aligned (W % 8 == 0)
     const uint32_t WB = warp_bytes(p.slice_words, BAR, TXT, kBmWordsT);
     uint64_t *tab_bar = reinterpret_cast<uint64_t *>(wbase + kMWarps * WB);
 
@@ -331,13 +378,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     fence_mbar_init();
     __syncthreads();
     if (tid == 0) {
-        const uint32_t jb = FBM ? kFBBytes : NJ * sizeof(CT), tb = p.window * 4 * sizeof(CT),
-                       fb = p.window * sizeof(CT);
+        const uint32_t jb = FBM ? kFBBytes : NJ * sizeof(CT), tb = p.window * kRowCells * sizeof(CT),
+                       fb = kMergedF ? 0u : p.window * (uint32_t)sizeof(CT);
         mbar_expect_tx(tab_bar, jb + tb + fb);
         bulk_g2s(smem, FBM ? (const void *)p.FB : p.J, jb, tab_bar);
         if (p.window) {
             bulk_g2s(sT, p.T, tb, tab_bar);
-            bulk_g2s(sF, p.F, fb, tab_bar);
+            if (fb) bulk_g2s(sF, p.F, fb, tab_bar);
         }
     }
     if (lane == 0 && s_first < s_end) issue(s_first, txt0, &bar[0]);
@@ -347,8 +394,12 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 
     uint32_t it = 0;
     uint64_t wcount = 0;   // fused: matches of this warp so far
-    uint32_t wstaged = 0;     // fused: of which staged (<= stg; the rest are streamed after the prefix)
+    uint32_t wstaged = 0;     // fused: of which staged (<= stg; the rest are logged or streamed after the prefix)
+    uint64_t wlogged = 0;     // fused: of which logged (slice records in the warp's match log)
+    uint64_t log_off = 0;     // fused: bytes of the warp's match log used
+    uint32_t emode = 0;       // fused: where this slice's matches go: 0 staging, 1 log, 2 spill (monotone)
     uint32_t spill_rel = ~0u; // fused: first spilled slice, relative to s_first
+    uint8_t *wlog = FUSE ? p.c.log + gw * p.c.log_pw : nullptr;
     bool bad_done = false;    // TXT: this warp has reported its first non-ACGT byte (slices ascend)
     uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
     uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
@@ -497,7 +548,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         const uint32_t i = lane + 32 * k;
                         l[k] = i < take ? queue[qb + i] : 0xFFFFu;
                         le[k] = (BAR && bar_slice && i < take) ? next_barrier(l[k]) : lend;
-                        g[k] = (i < take && l[k] + p.K2 <= le[k]) ? __ldg(p.J2 + (window16(txt, l[k]) & p.mask2))
+                        g[k] = (i < take && l[k] + p.K2 <= le[k]) ? ld_tab(p.J2 + (window16(txt, l[k]) & p.mask2))
                                                                    : 0xFFFFFFFFu;
                     }
 #pragma unroll
@@ -505,8 +556,20 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         if (l[k] == 0xFFFFu) continue;
                         uint32_t res;
                         if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], le[k]);  // near the end / a barrier
-                        else if (sizeof(CT) == 4 && p.HR && (g[k] & 0x40000000u))  // a chain head's row copy
-                            res = walk_head(tb, txt, __ldg(p.HR + (g[k] & 0x3FFFFFFFu)), l[k] + p.K2, le[k]);
+                        else if (sizeof(CT) == 4 && p.HR && (g[k] & kJ2HR)) {  // a chain head's row copy
+                            // NB entry: unless the next 4 bases are the chain's first 4 (and readable),
+                            // the walk ends inside the NOFIN span of an F = 0 head: the answer is 0
+                            // without the row load (builder.cpp, pfac_internal.h)
+                            const uint32_t l2 = l[k] + p.K2;
+                            if ((g[k] & kJ2NB) && (le[k] - l2 < kHRBases ||
+                                                   ((window16(txt, l2) ^ (g[k] >> kHRIndexBitsNB)) & 0xFFu)))
+                                res = 0;
+                            else
+                                res = walk_head(tb, txt,
+                                                ld_tab(p.HR + (g[k] & (g[k] & kJ2NB ? (1u << kHRIndexBitsNB) - 1
+                                                                                   : kJ2NB - 1))),
+                                                l2, le[k]);
+                        }
                         else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, le[k]);
                         else res = g[k];
                         if (!LIST || res) out[l[k]] = (int32_t)res;
@@ -530,6 +593,29 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
         // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
         auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3) {
+            // Common case (the group's positions fit the queue): one warp scan of the per-lane
+            // counts gives every lane its slots, and each lane writes its own positions -- no
+            // ballot round per queued position.
+            const uint32_t c = __popc(am);
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(~0u, incl, d);
+                if (lane >= (uint32_t)d) incl += y;
+            }
+            const uint32_t total = __shfl_sync(~0u, incl, 31);
+            if (kPushScan && qn + total <= kQCap) {
+                uint32_t slot = qn + incl - c;
+                while (am) {
+                    const uint32_t bit = __ffs(am) - 1;
+                    am &= am - 1;
+                    queue[slot++] =
+                        (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
+                }
+                qn += total;
+                drain(0);
+                return;
+            }
             while (true) {
                 const uint32_t b = __ballot_sync(~0u, am != 0);
                 if (!b) break;
@@ -755,9 +841,9 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
             }
             if (!cnt) {  // after a spill, list-only mode still needs this slice's (empty) bitmap
-                if (LIST && wstaged != wcount)
+                if (LIST && emode == 2)
                     for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = 0u;
-            } else if (wstaged == wcount && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
+            } else if (emode == 0 && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
 #pragma unroll 1
                 for (uint32_t w0 = 0; w0 < kBmWordsT; w0 += 32) {
                     uint32_t w = bm[w0 + lane];
@@ -780,10 +866,59 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     wcount += __shfl_sync(~0u, incl, 31);
                 }
                 wstaged = (uint32_t)wcount;
-            } else {  // the staging area is full: spill the slice's bitmap, emit it after the prefix
-                if (wstaged == wcount) spill_rel = (uint32_t)(sl - s_first);
-                if (LIST)  // out[] is valid only at matches: keep the slice's bitmap
-                    for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = bm[w];
+            } else {
+                const uint32_t pidb = p.c.pid16 ? 2u : 4u;
+                const uint32_t rec = log_record_bytes(kBmWordsT, cnt, pidb);
+                if (emode <= 1 && log_off + rec <= p.c.log_pw) {
+                    // the staging is full: log the slice -- [slice (relative), count, bitmap, pids] --
+                    // to be placed after the prefix without re-reading out[] (2-4 B per match + n/8)
+                    emode = 1;
+                    uint32_t *hdr = reinterpret_cast<uint32_t *>(wlog + log_off);
+                    uint32_t *lbm = hdr + 2;
+                    uint8_t *lpid = reinterpret_cast<uint8_t *>(lbm + kBmWordsT);
+                    if (lane == 0) {
+                        hdr[0] = (uint32_t)(sl - s_first);
+                        hdr[1] = cnt;
+                    }
+                    for (uint32_t w = lane; w < kBmWordsT; w += 32) lbm[w] = bm[w];
+                    // pids in position order, 128 positions per step: lane t owns positions 4t..4t+3
+                    // (one 16-byte read of the out[] cells this warp just wrote, L2 hits), ranks from
+                    // three ballots -- the stores of a step cover a contiguous rank range
+                    uint32_t run = 0;
+#pragma unroll 1
+                    for (uint32_t ch = 0; ch < kSliceT / 128; ++ch) {
+                        const uint32_t m = (bm[ch * 4 + (lane >> 3)] >> ((lane & 7) * 4)) & 0xFu;
+                        if (!__any_sync(~0u, m)) continue;
+                        uint32_t tot;
+                        uint32_t r = run + nibble_rank(m, lt, tot);
+                        if (m) {
+                            const uint32_t l0 = ch * 128 + lane * 4;
+                            uint32_t v[4];
+                            if (l0 + 4 <= lown) {
+                                const uint4 q = ld_cg_v4(out + l0);
+                                v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? ld_cg_u32(out + l0 + e) : 0u;
+                            }
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                if (!((m >> e) & 1)) continue;
+                                if (p.c.pid16) reinterpret_cast<uint16_t *>(lpid)[r] = (uint16_t)v[e];
+                                else reinterpret_cast<uint32_t *>(lpid)[r] = v[e];
+                                ++r;
+                            }
+                        }
+                        run += tot;
+                    }
+                    log_off += rec;
+                    wlogged += cnt;
+                } else {  // staging and log are full: spill, emit by re-reading out[] after the prefix
+                    if (emode != 2) spill_rel = (uint32_t)(sl - s_first);
+                    emode = 2;
+                    if (LIST)  // out[] is valid only at matches: keep the slice's bitmap
+                        for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = bm[w];
+                }
                 wcount += cnt;
             }
         }
@@ -794,14 +929,49 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
         const uint64_t prefix = grid_prefix<kMWarps>(wcount, p.c.counts, p.c.d_count, s_wcount, s_woff);
         for (uint64_t i = lane; i < wstaged; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);
+        // logged slices, in slice order: positions from each record's bitmap, pids from its list
+        __syncwarp();
+        uint64_t r0 = prefix + wstaged;
+        for (uint64_t off = 0; off < log_off;) {
+            const uint32_t *hdr = reinterpret_cast<const uint32_t *>(wlog + off);
+            const uint32_t rel = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr)),
+                           cnt = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr + 1));
+            const uint32_t *lbm = hdr + 2;
+            const uint8_t *lpid = reinterpret_cast<const uint8_t *>(lbm + kBmWordsT);
+            const uint64_t pbase = p.c.pos_base + (s_first + rel) * kSliceT;
+            uint32_t wr[kBmWordsT / 32];  // the record's bitmap, one word per lane and register
+#pragma unroll
+            for (uint32_t j = 0; j < kBmWordsT / 32; ++j)
+                wr[j] = ld_cg_u32(reinterpret_cast<const int32_t *>(lbm + j * 32 + lane));
+            uint32_t run = 0;
+#pragma unroll
+            for (uint32_t ch = 0; ch < kSliceT / 128; ++ch) {  // as in the emission: 4 positions per lane
+                const uint32_t m =
+                    (__shfl_sync(~0u, wr[ch * 4 / 32], (ch * 4 + (lane >> 3)) & 31) >> ((lane & 7) * 4)) & 0xFu;
+                if (!__any_sync(~0u, m)) continue;
+                uint32_t tot;
+                uint32_t r = run + nibble_rank(m, lt, tot);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (!((m >> e) & 1)) continue;
+                    const uint32_t v = p.c.pid16 ? (uint32_t)ld_cg_u16(reinterpret_cast<const uint16_t *>(lpid) + r)
+                                                 : ld_cg_u32(reinterpret_cast<const int32_t *>(lpid) + r);
+                    put_match(p.c, r0 + r, pbase + ch * 128 + lane * 4 + e, v);
+                    ++r;
+                }
+                run += tot;
+            }
+            r0 += cnt;
+            off += log_record_bytes(kBmWordsT, cnt, p.c.pid16 ? 2u : 4u);
+        }
         // spilled slices (dense matches): stream this warp's out[] from the first spilled slice
         // (list-only: masked by the spilled slice bitmaps, the scratch holds values only at matches)
-        if (wcount > wstaged) {
+        if (emode == 2) {
             const uint64_t spill_first = s_first + spill_rel;
             const uint64_t lo = spill_first * kSliceT < p.n_own ? spill_first * kSliceT : p.n_own;
             const uint64_t hi = s_end * kSliceT < p.n_own ? s_end * kSliceT : p.n_own;
             warp_stream<false>(
-                p.c, lo, hi, prefix + wstaged,
+                p.c, lo, hi, prefix + wstaged + wlogged,
                 [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); },
                 LIST ? p.c.bitmap : nullptr);
         }
@@ -831,6 +1001,7 @@ static void dev_props(int device, int &sms, int &optin) {
 #endif
 constexpr uint32_t kWindowMinShare = PFAC_WINDOW_MIN_SHARE;  // keep a row window only if rows <= this x window
 constexpr size_t kStaticSmemReserve = 1024;
+constexpr uint32_t kWinCells = kRowCells + (kMergedF ? 0 : 1);  // shared-memory cells per window row (T + F)
 #ifndef PFAC_TXT_MAX_ROWS
 #define PFAC_TXT_MAX_ROWS (1u << 20)
 #endif
@@ -839,7 +1010,7 @@ constexpr uint32_t kSliceSmall = 1024;  // the fused kernel's static shared arra
 
 static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
                          bool bar = false, bool txt = false, uint32_t bm_words = kBmWords) {
-    return table_bytes + (size_t)window * 5 * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt, bm_words) +
+    return table_bytes + (size_t)window * kWinCells * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt, bm_words) +
            16;
 }
 
@@ -852,7 +1023,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     const size_t table = h.K2 ? (size_t)kFBBytes : ((size_t)1 << (2 * h.K)) * pl.cell;
     const size_t fixed = match_smem(table, pl.cell, 0, pl.slice_words) + kStaticSmemReserve;
     const size_t budget = (size_t)optin > fixed ? (size_t)optin - fixed : 0;
-    uint32_t w = (uint32_t)(budget / (5 * pl.cell)) & ~7u;
+    uint32_t w = (uint32_t)(budget / (kWinCells * pl.cell)) & ~7u;
 #ifdef PFAC_WINDOW_MAX
     if (w > (uint32_t)(PFAC_WINDOW_MAX)) w = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
 #endif
@@ -867,7 +1038,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     // barrier-mode variant (BAR): per-warp barrier bits take room from the row window
     const size_t fixed_b = match_smem(table, pl.cell, 0, pl.slice_words, true) + kStaticSmemReserve;
     const size_t budget_b = (size_t)optin > fixed_b ? (size_t)optin - fixed_b : 0;
-    uint32_t wb = (uint32_t)(budget_b / (5 * pl.cell)) & ~7u;
+    uint32_t wb = (uint32_t)(budget_b / (kWinCells * pl.cell)) & ~7u;
     if (wb < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wb) wb = 0;
 #ifdef PFAC_WINDOW_MAX
     if (wb > (uint32_t)(PFAC_WINDOW_MAX)) wb = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
@@ -879,7 +1050,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     // only when the filter image fits beside them (halo <= 112 bases at 896 threads per CTA)
     const size_t fixed_t = match_smem(table, pl.cell, 0, pl.slice_words, true, true) + kStaticSmemReserve;
     pl.txt_ok = h.K2 != 0 && (size_t)optin >= fixed_t;
-    uint32_t wt = pl.txt_ok ? (uint32_t)(((size_t)optin - fixed_t) / (5 * pl.cell)) & ~7u : 0u;
+    uint32_t wt = pl.txt_ok ? (uint32_t)(((size_t)optin - fixed_t) / (kWinCells * pl.cell)) & ~7u : 0u;
     if (wt < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wt) wt = 0;
 #ifdef PFAC_WINDOW_MAX
     if (wt > (uint32_t)(PFAC_WINDOW_MAX)) wt = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
@@ -899,7 +1070,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     const size_t fixed_k = match_smem(table, pl.cell, 0, pl.slice_words_1k, true, true, kSliceSmall / 32) +
                            kStaticSmemReserve;
     pl.txt1k_ok = h.K2 != 0 && pl.cell == 4 && (size_t)optin >= fixed_k;
-    uint32_t wk = pl.txt1k_ok ? (uint32_t)(((size_t)optin - fixed_k) / (5 * pl.cell)) & ~7u : 0u;
+    uint32_t wk = pl.txt1k_ok ? (uint32_t)(((size_t)optin - fixed_k) / (kWinCells * pl.cell)) & ~7u : 0u;
     if (wk < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wk) wk = 0;
 #ifdef PFAC_WINDOW_MAX
     if (wk > (uint32_t)(PFAC_WINDOW_MAX)) wk = (uint32_t)(PFAC_WINDOW_MAX) & ~7u;
@@ -1083,6 +1254,9 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.stage_pid = reinterpret_cast<uint32_t *>(c.stage_pos + entries);
     c.bitmap = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_workspace) + kGMax * 8 +
                                             ((entries * 12 + 15) & ~15ull));
+    c.log = reinterpret_cast<uint8_t *>(c.bitmap) + spill_bitmap_bytes(n_own);
+    c.log_pw = (match_log_bytes(n_own) / warps) & ~15ull;
+    c.pid16 = k < 65536u;
     c.chunk = a.slices_per_warp * slice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;

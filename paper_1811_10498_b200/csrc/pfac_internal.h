@@ -34,6 +34,22 @@ constexpr int kK2Max = PFAC_K2MAX;  // largest second-level jump length (4^11 ce
 #endif
 constexpr int kK2Min = PFAC_K2MIN;  // smallest (>= kFilterK: the filter must not look further than J2)
 constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
+// Ablation (the paper's "two arrays vs one merged array"): PFAC_MERGED_F=1
+// stores F(s) in cell 4 of an 8-cell row next to the 4 transitions, so a walk that ends at a branch
+// state reads its answer from the row it already holds (rows twice as wide).  Default: T rows of 4
+// cells and the separate F array (chain rows carry F(s) in their spare cell either way).
+#ifndef PFAC_MERGED_F
+#define PFAC_MERGED_F 0
+#endif
+constexpr bool kMergedF = PFAC_MERGED_F;
+constexpr uint32_t kRowCells = kMergedF ? 8 : 4;
+// J2 entry encoding (uint32, the same for both cell widths): ALIVE | id of the depth-K2 state, or
+// the answer of a walk that dies within K2 bases.  uint32 images with chain-head copies (HR):
+//   ALIVE | HR | h                      -> the head's row is HR[h]   (h < 2^29)
+//   ALIVE | HR | NB | b4 << 21 | h      -> the same, and the row is a NOFIN chain of L >= 4 bases
+//                                          with F = 0 whose first 4 forced bases are b4 (h < 2^21)
+constexpr uint32_t kJ2Alive = 0x80000000u, kJ2HR = 0x40000000u, kJ2NB = 0x20000000u;
+constexpr uint32_t kHRBases = 4, kHRIndexBitsNB = 21;
 
 // Host-side device image: everything the match kernel reads, already in its cell width.
 //  * Device ids 1..S number the states deep-first and chain-major: first the states at depth >= K
@@ -67,6 +83,7 @@ struct HostImage {
     std::vector<uint32_t> FB;          // K2 > 0: 4^kFilterK-bit filter ("this K1-mer needs J2")
     std::vector<uint32_t> HR;          // uint32 images: copies of the depth-K2 chain-head T rows (4 cells,
                                        // cell 3 = the head's device id); J2 entry ALIVE|HRF|h points at row h
+    uint32_t hr_nb = 0;                // HR rows whose J2 entries use the NB form (kJ2NB)
 };
 
 // Launch plan of the match kernel for one automaton on one device (match.cu).

@@ -15,6 +15,9 @@ VARIANTS = {
     "window0": ["PFAC_WINDOW_MAX=0"],        # no transition-table rows in shared memory
     "jtable": ["PFAC_FB16=0"],               # uint16 images: 4^8 jump table instead of filter + J2
     "nopersist": ["PFAC_NO_PERSIST"],        # no L2 access-policy window over J2
+    "merged_f": ["PFAC_MERGED_F=1"],         # the paper's merged array: F(s) inside each T row
+    "tab_cg": ["PFAC_TAB_CG=1"],
+    "push_ballot": ["PFAC_PUSH_SCAN=0"],     # A/B: the round-1 queue push (one ballot round per position)             # table loads ld.global.cg (L2 only), the paper's -dlcm=cg
 }
 
 if __name__ == "__main__":

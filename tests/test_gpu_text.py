@@ -198,3 +198,53 @@ def test_text_empty():
     a = P.Automaton(SETS["cfg2like"]())
     out, pos, pid, m, fb = run_text(a, np.zeros(0, np.uint8))
     assert m == 0 and fb == -1
+
+
+def _prefixed_kmers(k: int, first: str) -> list[bytes]:
+    """All k-mers whose first base is in `first`: a share len(first)/4 of random-text positions match."""
+    return [p for p in gen.all_kmers(k) if chr(p[0]) in first]
+
+
+@pytest.mark.parametrize("width", ["u16", "u32"])
+@pytest.mark.parametrize("first", ["A", "AC"])
+@pytest.mark.parametrize("dense", [True, False], ids=["dense", "list"])
+def test_text_match_log(width, first, dense):
+    """Match densities of 25% / 50% over 24 Mbases: each warp's staging overflows after one slice, so
+    the next slices go through the per-warp match log (bitmap + pids, 2-byte pids when every id fits
+    in 16 bits, else 4-byte) and, where a slice's record no longer fits the log (50%, and 25% with
+    4-byte pids), the out[] re-read.  Lists and out[] must equal the oracle's (the list is in
+    position order across staged, logged and spilled slices)."""
+    pats = _prefixed_kmers(4 if width == "u16" else 9, first)
+    assert (len(pats) < 65536) == (width == "u16")
+    n = 24_000_000
+    text = gen.iid_text(300 + len(first), 0, n)
+    m = check(pats, text, dense=dense)
+    assert abs(m / n - 0.25 * len(first)) < 0.01
+
+
+@pytest.mark.parametrize("cut", range(-2, 8))
+def test_text_chain_heads_near_the_end(cut):
+    """uint32 images whose J2 entries carry a chain head's first 4 forced bases (the NB form): walks
+    that reach depth K2 with 0-3 bases left (the answer is 0 without the head's row), with exactly the
+    4 bases (row loaded), with a mismatch inside the first 4 (answer 0) and beyond them, and planted
+    complete patterns -- at the very end of the text and in its middle."""
+    pats = gen.random_patterns(204, 40_000, 24, 40)
+    a = P.Automaton(pats)
+    info = a.image_info(0)
+    assert info["cell_bytes"] == 4 and info["hr_nb_rows"] > 1000, info
+    K2 = info["K2"]
+    rng = np.random.default_rng(cut + 10)
+    pieces = []
+    for j in range(200):
+        p = np.frombuffer(pats[j], np.uint8).copy()
+        c = min(len(p), K2 + cut)
+        q = p[:c].copy()
+        if j % 3 == 1 and c > K2:  # a mismatch among the bases after depth K2
+            t = K2 + (j // 3) % (c - K2)
+            q[t] = b"ACGT"[(b"ACGT".index(q[t]) + 1) % 4]
+        pieces.append(gen.iid_text(1000 + j, 0, int(rng.integers(0, 40))))
+        pieces.append(q)
+    pieces.append(np.frombuffer(pats[7][:K2 + cut] if K2 + cut > 0 else b"", np.uint8))  # at the very end
+    text = np.concatenate(pieces)
+    check(pats, text)
+    check(pats, text, dense=False)
