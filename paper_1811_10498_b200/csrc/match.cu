@@ -140,19 +140,19 @@ struct Tab {
     uint32_t W;
     __device__ __forceinline__ Row<CT> row(uint32_t s) const {
         Row<CT> r;
-        const size_t b = (size_t)s * kRowCells;
         if constexpr (sizeof(CT) == 2 && kMergedF) {  // one 16-byte row: 4 transitions, F, padding
-            const uint4 v = (!WIN || s < W) ? *reinterpret_cast<const uint4 *>(Tw + b)
-                                            : ld_tab(reinterpret_cast<const uint4 *>(Tg + b));
+            const uint4 v = (!WIN || s < W) ? *reinterpret_cast<const uint4 *>(Tw + (size_t)s * kRowCells)
+                                            : ld_tab(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
             r.r = make_uint2(v.x, v.y);
             r.f = v.z & 0xFFFFu;
         } else if constexpr (sizeof(CT) == 2) {
-            if (!WIN || s < W) r.r = *reinterpret_cast<const uint2 *>(Tw + b);
-            else r.r = ld_tab(reinterpret_cast<const uint2 *>(Tg + b));
+            if (!WIN || s < W) r.r = *reinterpret_cast<const uint2 *>(Tw + (size_t)s * kRowCells);
+            else r.r = ld_tab(reinterpret_cast<const uint2 *>(Tg + (size_t)s * kRowCells));
         } else {
-            if (!WIN || s < W) r.r = *reinterpret_cast<const uint4 *>(Tw + b);
-            else r.r = ld_tab(reinterpret_cast<const uint4 *>(Tg + b));
-            if constexpr (kMergedF) r.f = (!WIN || s < W) ? (uint32_t)Tw[b + 4] : (uint32_t)ld_tab(Tg + b + 4);
+            if (!WIN || s < W) r.r = *reinterpret_cast<const uint4 *>(Tw + (size_t)s * kRowCells);
+            else r.r = ld_tab(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
+            if constexpr (kMergedF)
+                r.f = (!WIN || s < W) ? (uint32_t)Tw[(size_t)s * kRowCells + 4] : (uint32_t)ld_tab(Tg + (size_t)s * kRowCells + 4);
         }
         return r;
     }
@@ -270,6 +270,10 @@ constexpr uint32_t kQCap = 32 * kDrainIPL + 64;  // queue of flagged positions
 #define PFAC_PUSH_SCAN 1  // A/B knob: 0 = one ballot round per queued position per lane
 #endif
 constexpr bool kPushScan = PFAC_PUSH_SCAN;
+#ifndef PFAC_MATCH_LOG
+#define PFAC_MATCH_LOG 1  // A/B knob: 0 = no per-warp match log (a full staging area spills at once)
+#endif
+constexpr bool kMatchLog = PFAC_MATCH_LOG;
 constexpr int kFBK = kFilterK;                         // filter length K1 (FBM)
 constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared memory (4^10: 128 KiB)
 
@@ -394,12 +398,11 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 
     uint32_t it = 0;
     uint64_t wcount = 0;   // fused: matches of this warp so far
-    uint32_t wstaged = 0;     // fused: of which staged (<= stg; the rest are logged or streamed after the prefix)
-    uint64_t wlogged = 0;     // fused: of which logged (slice records in the warp's match log)
-    uint64_t log_off = 0;     // fused: bytes of the warp's match log used
-    uint32_t emode = 0;       // fused: where this slice's matches go: 0 staging, 1 log, 2 spill (monotone)
-    uint32_t spill_rel = ~0u; // fused: first spilled slice, relative to s_first
-    uint8_t *wlog = FUSE ? p.c.log + gw * p.c.log_pw : nullptr;
+    // fused: a slice's matches go to the staging area while it has room (wstaged == wcount), then
+    // to the warp's match log while that has room, then are spilled (re-read after the prefix)
+    uint32_t wstaged = 0;     // fused: matches staged (<= stg)
+    uint32_t log_off = 0;     // fused: bytes of the warp's match log used (< 2^32: log_pw ~ run length)
+    uint32_t spill_rel = ~0u; // fused: first spilled slice, relative to s_first (~0u: none)
     bool bad_done = false;    // TXT: this warp has reported its first non-ACGT byte (slices ascend)
     uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
     uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
@@ -593,9 +596,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
         // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
         auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3) {
-            // Common case (the group's positions fit the queue): one warp scan of the per-lane
-            // counts gives every lane its slots, and each lane writes its own positions -- no
-            // ballot round per queued position.
+            // One warp scan of the per-lane counts gives every lane the queue slots of its positions,
+            // and each lane writes its own -- no ballot round per queued position.
             const uint32_t c = __popc(am);
             uint32_t incl = c;
 #pragma unroll
@@ -604,15 +606,25 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 if (lane >= (uint32_t)d) incl += y;
             }
             const uint32_t total = __shfl_sync(~0u, incl, 31);
-            if (kPushScan && qn + total <= kQCap) {
-                uint32_t slot = qn + incl - c;
-                while (am) {
-                    const uint32_t bit = __ffs(am) - 1;
-                    am &= am - 1;
-                    queue[slot++] =
-                        (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
+            if (kPushScan) {
+                // the group's items have ranks [0, total), this lane's [excl, excl + c); each pass
+                // queues the ranks that fit the free room, then drains the full rounds
+                uint32_t r = incl - c, done = 0;
+                while (true) {
+                    const uint32_t hi = done + (kQCap - qn);  // ranks below hi fit this pass
+                    while (am && r < hi) {
+                        const uint32_t bit = __ffs(am) - 1;
+                        am &= am - 1;
+                        queue[qn + r - done] =
+                            (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
+                        ++r;
+                    }
+                    const uint32_t wrote = (total < hi ? total : hi) - done;
+                    qn += wrote;
+                    done += wrote;
+                    if (done == total) break;
+                    drain(qn & 31);  // keep < 32: every drained round is full
                 }
-                qn += total;
                 drain(0);
                 return;
             }
@@ -841,9 +853,9 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
             }
             if (!cnt) {  // after a spill, list-only mode still needs this slice's (empty) bitmap
-                if (LIST && emode == 2)
+                if (LIST && spill_rel != ~0u)
                     for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = 0u;
-            } else if (emode == 0 && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
+            } else if (wstaged == wcount && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
 #pragma unroll 1
                 for (uint32_t w0 = 0; w0 < kBmWordsT; w0 += 32) {
                     uint32_t w = bm[w0 + lane];
@@ -869,11 +881,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             } else {
                 const uint32_t pidb = p.c.pid16 ? 2u : 4u;
                 const uint32_t rec = log_record_bytes(kBmWordsT, cnt, pidb);
-                if (emode <= 1 && log_off + rec <= p.c.log_pw) {
+                if (spill_rel == ~0u && log_off + rec <= p.c.log_pw) {
                     // the staging is full: log the slice -- [slice (relative), count, bitmap, pids] --
                     // to be placed after the prefix without re-reading out[] (2-4 B per match + n/8)
-                    emode = 1;
-                    uint32_t *hdr = reinterpret_cast<uint32_t *>(wlog + log_off);
+                    uint32_t *hdr = reinterpret_cast<uint32_t *>(p.c.log + gw * p.c.log_pw + log_off);
                     uint32_t *lbm = hdr + 2;
                     uint8_t *lpid = reinterpret_cast<uint8_t *>(lbm + kBmWordsT);
                     if (lane == 0) {
@@ -912,10 +923,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         run += tot;
                     }
                     log_off += rec;
-                    wlogged += cnt;
                 } else {  // staging and log are full: spill, emit by re-reading out[] after the prefix
-                    if (emode != 2) spill_rel = (uint32_t)(sl - s_first);
-                    emode = 2;
+                    if (spill_rel == ~0u) spill_rel = (uint32_t)(sl - s_first);
                     if (LIST)  // out[] is valid only at matches: keep the slice's bitmap
                         for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = bm[w];
                 }
@@ -932,8 +941,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // logged slices, in slice order: positions from each record's bitmap, pids from its list
         __syncwarp();
         uint64_t r0 = prefix + wstaged;
-        for (uint64_t off = 0; off < log_off;) {
-            const uint32_t *hdr = reinterpret_cast<const uint32_t *>(wlog + off);
+        for (uint32_t off = 0; off < log_off;) {
+            const uint32_t *hdr = reinterpret_cast<const uint32_t *>(p.c.log + gw * p.c.log_pw + off);
             const uint32_t rel = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr)),
                            cnt = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr + 1));
             const uint32_t *lbm = hdr + 2;
@@ -943,11 +952,12 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 #pragma unroll
             for (uint32_t j = 0; j < kBmWordsT / 32; ++j)
                 wr[j] = ld_cg_u32(reinterpret_cast<const int32_t *>(lbm + j * 32 + lane));
+            static_assert(kBmWordsT == 32 || kBmWordsT == 64, "one or two bitmap words per lane");
             uint32_t run = 0;
-#pragma unroll
+#pragma unroll 1
             for (uint32_t ch = 0; ch < kSliceT / 128; ++ch) {  // as in the emission: 4 positions per lane
-                const uint32_t m =
-                    (__shfl_sync(~0u, wr[ch * 4 / 32], (ch * 4 + (lane >> 3)) & 31) >> ((lane & 7) * 4)) & 0xFu;
+                const uint32_t wsrc = ch >= 8 ? wr[kBmWordsT / 32 - 1] : wr[0];
+                const uint32_t m = (__shfl_sync(~0u, wsrc, (ch * 4 + (lane >> 3)) & 31) >> ((lane & 7) * 4)) & 0xFu;
                 if (!__any_sync(~0u, m)) continue;
                 uint32_t tot;
                 uint32_t r = run + nibble_rank(m, lt, tot);
@@ -966,12 +976,12 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         }
         // spilled slices (dense matches): stream this warp's out[] from the first spilled slice
         // (list-only: masked by the spilled slice bitmaps, the scratch holds values only at matches)
-        if (emode == 2) {
+        if (spill_rel != ~0u) {
             const uint64_t spill_first = s_first + spill_rel;
             const uint64_t lo = spill_first * kSliceT < p.n_own ? spill_first * kSliceT : p.n_own;
             const uint64_t hi = s_end * kSliceT < p.n_own ? s_end * kSliceT : p.n_own;
             warp_stream<false>(
-                p.c, lo, hi, prefix + wstaged + wlogged,
+                p.c, lo, hi, r0,  // after the staged and the logged matches
                 [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); },
                 LIST ? p.c.bitmap : nullptr);
         }
@@ -1255,7 +1265,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.bitmap = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_workspace) + kGMax * 8 +
                                             ((entries * 12 + 15) & ~15ull));
     c.log = reinterpret_cast<uint8_t *>(c.bitmap) + spill_bitmap_bytes(n_own);
-    c.log_pw = (match_log_bytes(n_own) / warps) & ~15ull;
+    c.log_pw = kMatchLog ? (match_log_bytes(n_own) / warps) & ~15ull : 0;
     c.pid16 = k < 65536u;
     c.chunk = a.slices_per_warp * slice;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
