@@ -265,7 +265,11 @@ constexpr bool kContiguousSchedule = PFAC_CONTIG;
 #define PFAC_DRAIN_IPL 1
 #endif
 constexpr uint32_t kDrainIPL = PFAC_DRAIN_IPL;  // queued items per lane per drain round (A/B knob)
-constexpr uint32_t kQCap = 32 * kDrainIPL + 64;  // queue of flagged positions
+// queue of flagged positions (entries per warp): the 1024-position-slice kernels (large automata,
+// ~9% of positions flagged: ~90 per 1024-position group) have the shared memory for a longer one
+static __host__ __device__ constexpr uint32_t qcap_for(uint32_t bm_words) {
+    return 32 * kDrainIPL + (bm_words <= 32 ? 160 : 64);
+}
 #ifndef PFAC_PUSH_SCAN
 #define PFAC_PUSH_SCAN 1  // A/B knob: 0 = one ballot round per queued position per lane
 #endif
@@ -284,9 +288,9 @@ static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, b
                                                          uint32_t bm_words = kBmWords) {
     // TXT: ASCII staging (slice_words * 16 bytes) + ONE packed slice and barrier-bit buffer (the warp
     // packs a slice before it prefetches the next one's bytes, so the ASCII buffer is the double buffer)
-    return txt ? slice_words * 16 + (slice_words + 4) * 4 + 16 + kQCap * 2 + bm_words * 4 +
+    return txt ? slice_words * 16 + (slice_words + 4) * 4 + 16 + qcap_for(bm_words) * 2 + bm_words * 4 +
                      inv_buf_words(slice_words) * 2
-               : 2 * (slice_words + 4) * 4 + 16 + kQCap * 2 + bm_words * 4 +  // text, mbarriers, queue, bitmap
+               : 2 * (slice_words + 4) * 4 + 16 + qcap_for(bm_words) * 2 + bm_words * 4 +  // text, mbarriers, queue, bitmap
                      (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);          // BAR: the slice's barrier bits
 }
 
@@ -295,7 +299,7 @@ template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, b
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // positions per slice (text kernel for large automata: 1024, which leaves L1 more room)
     static_assert(SL % 1024 == 0 && SL <= 65536, "slice = whole 1024-position groups, u16 positions");
-    constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32;
+    constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32, kQCap = qcap_for(SL / 32);
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
@@ -606,28 +610,19 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 if (lane >= (uint32_t)d) incl += y;
             }
             const uint32_t total = __shfl_sync(~0u, incl, 31);
-            if (kPushScan) {
-                // the group's items have ranks [0, total), this lane's [excl, excl + c); each pass
-                // queues the ranks that fit the free room, then drains the full rounds
-                uint32_t r = incl - c, done = 0;
-                while (true) {
-                    const uint32_t hi = done + (kQCap - qn);  // ranks below hi fit this pass
-                    while (am && r < hi) {
-                        const uint32_t bit = __ffs(am) - 1;
-                        am &= am - 1;
-                        queue[qn + r - done] =
-                            (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
-                        ++r;
-                    }
-                    const uint32_t wrote = (total < hi ? total : hi) - done;
-                    qn += wrote;
-                    done += wrote;
-                    if (done == total) break;
-                    drain(qn & 31);  // keep < 32: every drained round is full
+            if (kPushScan && qn + total <= kQCap) {  // the group fits: each lane writes its own
+                uint32_t slot = qn + incl - c;
+                while (am) {
+                    const uint32_t bit = __ffs(am) - 1;
+                    am &= am - 1;
+                    queue[slot++] =
+                        (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
                 }
+                qn += total;
                 drain(0);
                 return;
             }
+            // dense groups (repetitive text): one queued position per lane and ballot round
             while (true) {
                 const uint32_t b = __ballot_sync(~0u, am != 0);
                 if (!b) break;
@@ -881,7 +876,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             } else {
                 const uint32_t pidb = p.c.pid16 ? 2u : 4u;
                 const uint32_t rec = log_record_bytes(kBmWordsT, cnt, pidb);
-                if (spill_rel == ~0u && log_off + rec <= p.c.log_pw) {
+                if (kMatchLog && spill_rel == ~0u && log_off + rec <= p.c.log_pw) {
                     // the staging is full: log the slice -- [slice (relative), count, bitmap, pids] --
                     // to be placed after the prefix without re-reading out[] (2-4 B per match + n/8)
                     uint32_t *hdr = reinterpret_cast<uint32_t *>(p.c.log + gw * p.c.log_pw + log_off);
@@ -941,7 +936,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // logged slices, in slice order: positions from each record's bitmap, pids from its list
         __syncwarp();
         uint64_t r0 = prefix + wstaged;
-        for (uint32_t off = 0; off < log_off;) {
+        for (uint32_t off = 0; kMatchLog && off < log_off;) {
             const uint32_t *hdr = reinterpret_cast<const uint32_t *>(p.c.log + gw * p.c.log_pw + off);
             const uint32_t rel = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr)),
                            cnt = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr + 1));

@@ -16,10 +16,11 @@ VARIANTS = {
     "jtable": ["PFAC_FB16=0"],               # uint16 images: 4^8 jump table instead of filter + J2
     "nopersist": ["PFAC_NO_PERSIST"],        # no L2 access-policy window over J2
     "merged_f": ["PFAC_MERGED_F=1"],         # the paper's merged array: F(s) inside each T row
-    "tab_cg": ["PFAC_TAB_CG=1"],
-    "push_ballot": ["PFAC_PUSH_SCAN=0"],
-    "nolog": ["PFAC_MATCH_LOG=0"],
-    "ipl2": ["PFAC_DRAIN_IPL=2"],            # A/B: two queued positions per lane per drain round           # A/B: dense matches spill straight to the out[] re-read     # A/B: the round-1 queue push (one ballot round per position)             # table loads ld.global.cg (L2 only), the paper's -dlcm=cg
+    "tab_cg": ["PFAC_TAB_CG=1"],             # table loads ld.global.cg (L2 only), the paper's -dlcm=cg
+    "push_ballot": ["PFAC_PUSH_SCAN=0"],     # A/B: the round-1 queue push (one ballot round per position)
+    "nolog": ["PFAC_MATCH_LOG=0"],           # A/B: no match log (dense matches spill to the out[] re-read)
+    "nolog_ballot": ["PFAC_MATCH_LOG=0", "PFAC_PUSH_SCAN=0"],
+    "ipl2": ["PFAC_DRAIN_IPL=2"],            # A/B: two queued positions per lane per drain round
 }
 
 if __name__ == "__main__":

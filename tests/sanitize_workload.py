@@ -81,7 +81,37 @@ def run(pats, text, tag):
     check(hm == len(epos) and (hp.numpy() == epos).all(), f"{tag} scan_host")
 
 
+def run_log(pats, text, tag):
+    """The fused and text kernels on a text long enough (and dense enough: every position whose
+    first base is in a set matches) that each warp's staging overflows and its slices go through the
+    per-warp match log and, when that is full, the out[] re-read (match.cu, FUSE emission)."""
+    n = len(text)
+    epos, epid = Oracle(pats).match_list(text)
+    a = P.Automaton(pats)
+    d = torch.from_numpy(text).to(DEV)
+    cap = len(epos) + 16
+    pos = torch.empty(cap, dtype=torch.int64, device=DEV)
+    pid = torch.empty(cap, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    for mode in (0, 1):
+        a.set_text_kernel(mode)
+        for dense in (True, False):
+            wst = torch.empty(P.match_text_workspace_bytes(n, n, not dense), dtype=torch.uint8, device=DEV)
+            o3 = torch.empty(n, dtype=torch.int32, device=DEV) if dense else None
+            P.match_text_async(a, d, n, n, o3, pos, pid, cnt, wst)
+            torch.cuda.synchronize()
+            check(int(cnt.item()) == len(epos) and (pos[:len(epos)].cpu().numpy() == epos).all()
+                  and (pid[:len(epos)].cpu().numpy() == epid).all(), f"{tag} text mode {mode} dense {dense}")
+
+
 def main():
+    if os.environ.get("PFAC_SANITIZE_LOG"):
+        n = int(os.environ.get("PFAC_SANITIZE_LOG_N", "24000000"))
+        for k, first in ((4, "A"), (4, "AC"), (9, "A")):
+            pats = [p for p in gen.all_kmers(k) if chr(p[0]) in first]
+            run_log(pats, gen.iid_text(300 + k, 0, n), f"log k={k} first={first}")
+        print("sanitize_workload ok")
+        return
     n = int(os.environ.get("PFAC_SANITIZE_N", "70001"))
     cfg1 = gen.config_patterns(gen.CONFIGS[1])
     big = gen.random_patterns(41, 40_000, 12, 40)  # uint32 image, J2 + chain-head rows

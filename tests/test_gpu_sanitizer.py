@@ -23,11 +23,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck", "memcheck-log"])
 def test_sanitizer_clean(tool):
+    """memcheck-log: memcheck over 24-Mbase dense texts (the fused kernels' match-log and spill paths)."""
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not found")
     env = dict(os.environ, PFAC_SANITIZE_N="70001" if tool == "memcheck" else "20001")
+    if tool == "memcheck-log":
+        tool = "memcheck"
+        env["PFAC_SANITIZE_LOG"] = "1"
     extra = ["--racecheck-report", "all"] if tool == "racecheck" else []
     cmd = [SAN, "--tool", tool, *extra, "--error-exitcode", "99", "--print-limit", "20",
            sys.executable, os.path.join(ROOT, "tests", "sanitize_workload.py")]
