@@ -75,6 +75,10 @@ static int get_image(const pfac_automaton *ca, int device, DeviceImage **out) {
     im->maxlen = a->maxlen;
     im->minlen = a->minlen;
     im->short_pat = h.short_pat;
+    if (!fb_addressing_ok(device)) {
+        delete im;
+        return fail(PFAC_E_CUDA, "device image: unexpected reserved shared memory per block (match.cu kFBSmemBase)");
+    }
     im->plan = plan_match(device, h, a->maxlen);
     // One allocation [J2 | T | F | J | FB] (256-byte aligned parts); the L2 access-policy window
     // covers the J2 prefix.

@@ -153,12 +153,14 @@ __device__ __forceinline__ void put_match(const CompactArgs &a, uint64_t r, uint
 // (a slice is <= 65536 positions), 16-byte multiple.
 inline uint64_t spill_bitmap_bytes(uint64_t n) { return (((n + 65536) / 32) * 4 + 15) & ~15ull; }
 
-// The fused kernels' per-warp match logs: 1 byte per position (a slice's record -- its match bitmap
-// and the pids of its matches -- costs 8 + n/8 + 2 or 4 bytes per match, so the log holds every
-// slice of a warp's run up to ~43% (uint16 pids) / ~22% (uint32) match density; denser runs spill).
-inline uint64_t match_log_bytes(uint64_t n) { return (n + 15) & ~15ull; }
-__host__ __device__ constexpr uint32_t log_record_bytes(uint32_t bm_words, uint32_t cnt, uint32_t pid_bytes) {
-    return (8 + bm_words * 4 + cnt * pid_bytes + 15) & ~15u;
+// The fused kernels' per-warp match logs: a slice's record is a header (slice, count) and one entry
+// per match in position order -- (offset in the slice | pid << 16) as 4 bytes when every id fits in
+// 16 bits, else (offset, pid) as 8 bytes -- so placing it after the prefix is a coalesced copy.
+// 5/4 bytes per position: every slice of a warp's run fits up to ~31% (4-byte entries) / ~15%
+// (8-byte) match density; denser runs spill their remaining slices to the out[] re-read.
+inline uint64_t match_log_bytes(uint64_t n) { return (n + n / 4 + 15) & ~15ull; }
+__host__ __device__ constexpr uint32_t log_record_bytes(uint32_t cnt, uint32_t entry_bytes) {
+    return (16 + cnt * entry_bytes + 15) & ~15u;
 }
 
 inline uint64_t stage_entries(uint64_t n) {

@@ -178,6 +178,31 @@ __device__ __forceinline__ uint32_t nibble_rank(uint32_t m, uint32_t lt, uint32_
     return __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
 }
 
+#ifndef PFAC_FB_LOP
+#define PFAC_FB_LOP 1  // A/B knob: 0 = filter word address as base + offset (an extra IADD per lookup)
+#endif
+// Shared-window offset of the dynamic shared memory when the kernel has no static shared memory:
+// the 1 KiB the system reserves per block comes first (cudaDevAttrReservedSharedMemoryPerBlock,
+// checked by plan_match).
+constexpr uint32_t kFBSmemBase = 1024;
+constexpr bool kFbLop = PFAC_FB_LOP && kFilterK == 10;  // the 0x1FFFC mask is FB's 128 KiB
+
+bool fb_addressing_ok(int device) {
+    int reserved = -1;
+    if (cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device) != cudaSuccess) return false;
+    return !kFbLop || (uint32_t)reserved == kFBSmemBase;
+}
+
+// The 4-byte filter word at byte offset (y & 0x1FFFC) of FB, the first 128 KiB of the dynamic shared
+// memory: hi = the shared-window address of the dynamic region with its low 17 bits cleared, so the
+// address is one LOP3 ((y & 0x1FFFC) | hi) and the region's base rides in the load's immediate.
+__device__ __forceinline__ uint32_t lds_fb(uint32_t hi, uint32_t y) {
+    uint32_t a, v;
+    asm("lop3.b32 %0, %1, 0x1FFFC, %2, 0xEA;" : "=r"(a) : "r"(y), "r"(hi));
+    asm volatile("ld.shared.u32 %0, [%1+1024];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 // 16 bases starting at local offset l (base i in bits 2i).
 __device__ __forceinline__ uint32_t window16(const uint32_t *txt, uint32_t l) {
     const uint32_t q = l >> 4;
@@ -299,7 +324,8 @@ template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, b
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // positions per slice (text kernel for large automata: 1024, which leaves L1 more room)
     static_assert(SL % 1024 == 0 && SL <= 65536, "slice = whole 1024-position groups, u16 positions");
-    constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32, kQCap = qcap_for(SL / 32);
+    constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32;
+    constexpr uint32_t kQCap = qcap_for(kBmWordsT);
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
@@ -307,7 +333,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
     static_assert(kP + K - 1 <= 16, "the eight K-mers of a lane come from one 32-bit window");
-    constexpr uint32_t FBMASK = (1u << (2 * kFBK)) - 1;
+    [[maybe_unused]] constexpr uint32_t FBMASK = (1u << (2 * kFBK)) - 1;
     extern __shared__ __align__(128) uint8_t smem[];
     CT *sJ = reinterpret_cast<CT *>(smem);                 // J (4^K cells) ...
     const uint32_t *sFB = reinterpret_cast<const uint32_t *>(smem);  // ... or, FBM: the K1-mer filter
@@ -327,7 +353,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint16_t *inv0 = reinterpret_cast<uint16_t *>(bm + kBmWordsT);  // BAR: barrier bits of the slice
     uint16_t *inv1 = TXT ? inv0 : inv0 + inv_buf_words(p.slice_words);
     const uint32_t lt = (1u << lane) - 1;
-    __shared__ uint64_t s_wcount[kMWarps], s_woff[kMWarps];
+    // grid_prefix's per-warp counts live in the dynamic region too: with no static shared memory the
+    // dynamic region (FB first) starts right after the 1 KiB the system reserves, which the filter
+    // lookups' addressing relies on (fb_word)
+    uint64_t *s_wcount = tab_bar + 1, *s_woff = tab_bar + 1 + kMWarps;
+    uint32_t fb_hi = 0;
+    if constexpr (kFbLop) {
+        const uint32_t fb_sa = (uint32_t)__cvta_generic_to_shared(smem);
+        if ((fb_sa & 0x1FFFFu) != kFBSmemBase) __trap();  // host-checked (fb_addressing_ok); never taken
+        fb_hi = fb_sa & ~0x1FFFFu;
+    }
+    // the filter word of K1-mer bits [sh, sh + 2 K1) of x: bit (x >> sh) & 31 of word (x >> (sh + 5))
+    auto fb_word = [&](uint64_t x, uint32_t sh) -> uint32_t {
+        if constexpr (kFbLop) return lds_fb(fb_hi, (uint32_t)(x >> (sh + 3)));
+        else return sFB[((uint32_t)(x >> sh) & FBMASK) >> 5];
+    };
 
     const uint64_t TW = (uint64_t)gridDim.x * kMWarps;
     const uint64_t gw = (uint64_t)blockIdx.x * kMWarps + warp;
@@ -649,10 +689,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 const uint64_t x64 = (((uint64_t)txt[q + 1]) << 32) | txt[q];
                 uint32_t m = 0;
 #pragma unroll
-                for (uint32_t j = 0; j < 16; ++j) {
-                    const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
-                    m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
-                }
+                for (uint32_t j = 0; j < 16; ++j)
+                    m |= ((fb_word(x64, 2 * j) >> ((uint32_t)(x64 >> (2 * j)) & 31)) & 1u) << j;
                 if constexpr (!LIST) {
                     const uint32_t z0 = hg * 1024 + r * 512 + lane * 4;
 #pragma unroll
@@ -695,10 +733,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     }
                     } else {
 #pragma unroll
-                    for (uint32_t j = 0; j < kP; ++j) {
-                        const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
-                        m |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
-                    }
+                    for (uint32_t j = 0; j < kP; ++j)
+                        m |= ((fb_word(x64, 2 * j) >> ((uint32_t)(x64 >> (2 * j)) & 31)) & 1u) << j;
                     }
                     if constexpr (!LIST) {  // the sub-slice's zeros: every store is zeros, so the warp
                         // writes two contiguous 512-B runs (A/B knob: each lane its own 8 positions)
@@ -756,10 +792,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     // fits before it, out = 0.  Both as smears of the barrier bits, branch-free.
                     uint32_t fb = 0, near = 0, dead = 0;
 #pragma unroll
-                    for (uint32_t j = 0; j < kP; ++j) {
-                        const uint32_t idx = (uint32_t)(x64 >> (2 * j)) & FBMASK;
-                        fb |= ((sFB[idx >> 5] >> (idx & 31)) & 1u) << j;
-                    }
+                    for (uint32_t j = 0; j < kP; ++j)
+                        fb |= ((fb_word(x64, 2 * j) >> ((uint32_t)(x64 >> (2 * j)) & 31)) & 1u) << j;
 #pragma unroll
                     for (uint32_t t = 0; t < (uint32_t)kFBK; ++t) {
                         near |= ib >> t;
@@ -874,22 +908,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 }
                 wstaged = (uint32_t)wcount;
             } else {
-                const uint32_t pidb = p.c.pid16 ? 2u : 4u;
-                const uint32_t rec = log_record_bytes(kBmWordsT, cnt, pidb);
+                const uint32_t eb = p.c.pid16 ? 4u : 8u;
+                const uint32_t rec = log_record_bytes(cnt, eb);
                 if (kMatchLog && spill_rel == ~0u && log_off + rec <= p.c.log_pw) {
-                    // the staging is full: log the slice -- [slice (relative), count, bitmap, pids] --
-                    // to be placed after the prefix without re-reading out[] (2-4 B per match + n/8)
+                    // the staging is full: log the slice -- header [slice (relative), count], then
+                    // (offset, pid) per match in position order -- to be placed after the prefix by a
+                    // coalesced copy instead of re-reading out[]
                     uint32_t *hdr = reinterpret_cast<uint32_t *>(p.c.log + gw * p.c.log_pw + log_off);
-                    uint32_t *lbm = hdr + 2;
-                    uint8_t *lpid = reinterpret_cast<uint8_t *>(lbm + kBmWordsT);
+                    uint32_t *ent = hdr + 4;
                     if (lane == 0) {
                         hdr[0] = (uint32_t)(sl - s_first);
                         hdr[1] = cnt;
                     }
-                    for (uint32_t w = lane; w < kBmWordsT; w += 32) lbm[w] = bm[w];
-                    // pids in position order, 128 positions per step: lane t owns positions 4t..4t+3
-                    // (one 16-byte read of the out[] cells this warp just wrote, L2 hits), ranks from
-                    // three ballots -- the stores of a step cover a contiguous rank range
+                    // 128 positions per step: lane t owns positions 4t..4t+3 (one 16-byte read of the
+                    // out[] cells this warp just wrote, L2 hits); ranks from three ballots, so a step's
+                    // stores cover a contiguous rank range
                     uint32_t run = 0;
 #pragma unroll 1
                     for (uint32_t ch = 0; ch < kSliceT / 128; ++ch) {
@@ -908,10 +941,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                                 for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? ld_cg_u32(out + l0 + e) : 0u;
                             }
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
+                            for (uint32_t e = 0; e < 4; ++e) {
                                 if (!((m >> e) & 1)) continue;
-                                if (p.c.pid16) reinterpret_cast<uint16_t *>(lpid)[r] = (uint16_t)v[e];
-                                else reinterpret_cast<uint32_t *>(lpid)[r] = v[e];
+                                if (p.c.pid16) ent[r] = (l0 + e) | (v[e] << 16);
+                                else reinterpret_cast<uint2 *>(ent)[r] = make_uint2(l0 + e, v[e]);
                                 ++r;
                             }
                         }
@@ -940,34 +973,23 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             const uint32_t *hdr = reinterpret_cast<const uint32_t *>(p.c.log + gw * p.c.log_pw + off);
             const uint32_t rel = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr)),
                            cnt = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr + 1));
-            const uint32_t *lbm = hdr + 2;
-            const uint8_t *lpid = reinterpret_cast<const uint8_t *>(lbm + kBmWordsT);
+            const uint32_t *ent = hdr + 4;
             const uint64_t pbase = p.c.pos_base + (s_first + rel) * kSliceT;
-            uint32_t wr[kBmWordsT / 32];  // the record's bitmap, one word per lane and register
-#pragma unroll
-            for (uint32_t j = 0; j < kBmWordsT / 32; ++j)
-                wr[j] = ld_cg_u32(reinterpret_cast<const int32_t *>(lbm + j * 32 + lane));
-            static_assert(kBmWordsT == 32 || kBmWordsT == 64, "one or two bitmap words per lane");
-            uint32_t run = 0;
-#pragma unroll 1
-            for (uint32_t ch = 0; ch < kSliceT / 128; ++ch) {  // as in the emission: 4 positions per lane
-                const uint32_t wsrc = ch >= 8 ? wr[kBmWordsT / 32 - 1] : wr[0];
-                const uint32_t m = (__shfl_sync(~0u, wsrc, (ch * 4 + (lane >> 3)) & 31) >> ((lane & 7) * 4)) & 0xFu;
-                if (!__any_sync(~0u, m)) continue;
-                uint32_t tot;
-                uint32_t r = run + nibble_rank(m, lt, tot);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (!((m >> e) & 1)) continue;
-                    const uint32_t v = p.c.pid16 ? (uint32_t)ld_cg_u16(reinterpret_cast<const uint16_t *>(lpid) + r)
-                                                 : ld_cg_u32(reinterpret_cast<const int32_t *>(lpid) + r);
-                    put_match(p.c, r0 + r, pbase + ch * 128 + lane * 4 + e, v);
-                    ++r;
+            if (p.c.pid16) {
+#pragma unroll 4
+                for (uint32_t i = lane; i < cnt; i += 32) {
+                    const uint32_t e = ld_cg_u32(reinterpret_cast<const int32_t *>(ent + i));
+                    put_match(p.c, r0 + i, pbase + (e & 0xFFFFu), e >> 16);
                 }
-                run += tot;
+            } else {
+#pragma unroll 4
+                for (uint32_t i = lane; i < cnt; i += 32) {
+                    const uint2 e = __ldcg(reinterpret_cast<const uint2 *>(ent) + i);
+                    put_match(p.c, r0 + i, pbase + e.x, e.y);
+                }
             }
             r0 += cnt;
-            off += log_record_bytes(kBmWordsT, cnt, p.c.pid16 ? 2u : 4u);
+            off += log_record_bytes(cnt, p.c.pid16 ? 4u : 8u);
         }
         // spilled slices (dense matches): stream this warp's out[] from the first spilled slice
         // (list-only: masked by the spilled slice bitmaps, the scratch holds values only at matches)
@@ -1016,7 +1038,7 @@ constexpr uint32_t kSliceSmall = 1024;  // the fused kernel's static shared arra
 static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
                          bool bar = false, bool txt = false, uint32_t bm_words = kBmWords) {
     return table_bytes + (size_t)window * kWinCells * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt, bm_words) +
-           16;
+           16 + 2 * kMWarps * 8;  // + the table mbarrier and grid_prefix's per-warp counts
 }
 
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {

@@ -110,6 +110,10 @@ struct MatchPlan {
     int sms = 0;
 };
 
+// The match kernel's filter lookups assume the dynamic shared memory starts right after the
+// per-block reserved region (match.cu, kFBSmemBase); false if this device reserves another size.
+bool fb_addressing_ok(int device);
+
 struct ScanCtx;  // pfac_scan_host pipeline resources (api.cu)
 void free_scan_ctx(ScanCtx *c);
 

@@ -21,6 +21,7 @@ VARIANTS = {
     "nolog": ["PFAC_MATCH_LOG=0"],           # A/B: no match log (dense matches spill to the out[] re-read)
     "nolog_ballot": ["PFAC_MATCH_LOG=0", "PFAC_PUSH_SCAN=0"],
     "ipl2": ["PFAC_DRAIN_IPL=2"],            # A/B: two queued positions per lane per drain round
+    "fb_add": ["PFAC_FB_LOP=0"],             # A/B: filter word addresses as base + offset (one more IADD per lookup)
 }
 
 if __name__ == "__main__":
