@@ -289,11 +289,18 @@ constexpr bool kContiguousSchedule = PFAC_CONTIG;
 #ifndef PFAC_DRAIN_IPL
 #define PFAC_DRAIN_IPL 1
 #endif
-constexpr uint32_t kDrainIPL = PFAC_DRAIN_IPL;  // queued items per lane per drain round (A/B knob)
+#ifndef PFAC_DRAIN_IPL_1K
+#define PFAC_DRAIN_IPL_1K 2
+#endif
+// queued items per lane per drain round (A/B knobs): two for the 1024-position-slice kernels (large
+// automata: J2 latency; cfg4 -3%), one elsewhere (cfg2/cfg3 +1% with two)
+static __host__ __device__ constexpr uint32_t drain_ipl_for(uint32_t bm_words) {
+    return bm_words <= 32 ? PFAC_DRAIN_IPL_1K : PFAC_DRAIN_IPL;
+}
 // queue of flagged positions (entries per warp): the 1024-position-slice kernels (large automata,
 // ~9% of positions flagged: ~90 per 1024-position group) have the shared memory for a longer one
 static __host__ __device__ constexpr uint32_t qcap_for(uint32_t bm_words) {
-    return 32 * kDrainIPL + (bm_words <= 32 ? 160 : 64);
+    return 32 * drain_ipl_for(bm_words) + (bm_words <= 32 ? 160 : 64);
 }
 #ifndef PFAC_PUSH_SCAN
 #define PFAC_PUSH_SCAN 1  // A/B knob: 0 = one ballot round per queued position per lane
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // positions per slice (text kernel for large automata: 1024, which leaves L1 more room)
     static_assert(SL % 1024 == 0 && SL <= 65536, "slice = whole 1024-position groups, u16 positions");
     constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32;
-    constexpr uint32_t kQCap = qcap_for(kBmWordsT);
+    constexpr uint32_t kQCap = qcap_for(kBmWordsT), kDrainIPL = drain_ipl_for(kBmWordsT);
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
@@ -933,12 +940,14 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         if (m) {
                             const uint32_t l0 = ch * 128 + lane * 4;
                             uint32_t v[4];
+                            // (__ldcg: L2, coherent with this warp's stores before the __syncwarp above,
+                            // and not volatile, so the loads of a step can overlap the log stores)
                             if (l0 + 4 <= lown) {
-                                const uint4 q = ld_cg_v4(out + l0);
+                                const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(out + l0));
                                 v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
                             } else {
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? ld_cg_u32(out + l0 + e) : 0u;
+                                for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? (uint32_t)__ldcg(out + l0 + e) : 0u;
                             }
 #pragma unroll
                             for (uint32_t e = 0; e < 4; ++e) {
@@ -971,14 +980,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         uint64_t r0 = prefix + wstaged;
         for (uint32_t off = 0; kMatchLog && off < log_off;) {
             const uint32_t *hdr = reinterpret_cast<const uint32_t *>(p.c.log + gw * p.c.log_pw + off);
-            const uint32_t rel = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr)),
-                           cnt = ld_cg_u32(reinterpret_cast<const int32_t *>(hdr + 1));
+            const uint32_t rel = __ldcg(hdr), cnt = __ldcg(hdr + 1);  // this warp's own log (coherent L2 loads)
             const uint32_t *ent = hdr + 4;
             const uint64_t pbase = p.c.pos_base + (s_first + rel) * kSliceT;
             if (p.c.pid16) {
 #pragma unroll 4
                 for (uint32_t i = lane; i < cnt; i += 32) {
-                    const uint32_t e = ld_cg_u32(reinterpret_cast<const int32_t *>(ent + i));
+                    const uint32_t e = __ldcg(ent + i);
                     put_match(p.c, r0 + i, pbase + (e & 0xFFFFu), e >> 16);
                 }
             } else {

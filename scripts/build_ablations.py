@@ -20,7 +20,8 @@ VARIANTS = {
     "push_ballot": ["PFAC_PUSH_SCAN=0"],     # A/B: the round-1 queue push (one ballot round per position)
     "nolog": ["PFAC_MATCH_LOG=0"],           # A/B: no match log (dense matches spill to the out[] re-read)
     "nolog_ballot": ["PFAC_MATCH_LOG=0", "PFAC_PUSH_SCAN=0"],
-    "ipl2": ["PFAC_DRAIN_IPL=2"],            # A/B: two queued positions per lane per drain round
+    "ipl2": ["PFAC_DRAIN_IPL=2"],            # A/B: two queued positions per lane per drain round (2048-position slices too)
+    "ipl1": ["PFAC_DRAIN_IPL_1K=1"],         # A/B: one per lane in the 1024-position-slice kernels too
     "fb_add": ["PFAC_FB_LOP=0"],             # A/B: filter word addresses as base + offset (one more IADD per lookup)
 }
 
