@@ -647,18 +647,23 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
         // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
         auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3) {
-            // One warp scan of the per-lane counts gives every lane the queue slots of its positions,
-            // and each lane writes its own -- no ballot round per queued position.
+            // The lanes' slots are the exclusive prefix of their counts c, from ballots of the bits of c
+            // (independent instructions, no shuffle chain): two when every c <= 3 (sparse groups),
+            // six otherwise (c <= 32).  Each lane then writes its own positions -- no ballot round
+            // per queued position.
             const uint32_t c = __popc(am);
-            uint32_t incl = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(~0u, incl, d);
-                if (lane >= (uint32_t)d) incl += y;
+            uint32_t excl = 0, total = 0;
+            if (kPushScan) {
+                const uint32_t nb = __ballot_sync(~0u, c > 3) ? 6 : 2;
+                for (uint32_t k = 0; k < nb; ++k) {
+                    const uint32_t b = __ballot_sync(~0u, (c >> k) & 1u);
+                    excl += __popc(b & lt) << k;
+                    total += __popc(b) << k;
+                }
+                if (total == 0) return;
             }
-            const uint32_t total = __shfl_sync(~0u, incl, 31);
             if (kPushScan && qn + total <= kQCap) {  // the group fits: each lane writes its own
-                uint32_t slot = qn + incl - c;
+                uint32_t slot = qn + excl;
                 while (am) {
                     const uint32_t bit = __ffs(am) - 1;
                     am &= am - 1;
@@ -931,33 +936,39 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     // out[] cells this warp just wrote, L2 hits); ranks from three ballots, so a step's
                     // stores cover a contiguous rank range
                     uint32_t run = 0;
+                    // the out[] cells of the next step are loaded while this step is written (__ldcg: L2,
+                    // coherent with this warp's stores before the __syncwarp above; not volatile)
+                    auto ld4 = [&](uint32_t ch) -> uint4 {
+                        const uint32_t l0 = ch * 128 + lane * 4;
+                        return ch < kSliceT / 128 && l0 + 4 <= lown ? __ldcg(reinterpret_cast<const uint4 *>(out + l0))
+                                                                    : make_uint4(0, 0, 0, 0);
+                    };
+                    uint4 q = ld4(0);
 #pragma unroll 1
                     for (uint32_t ch = 0; ch < kSliceT / 128; ++ch) {
+                        const uint4 qn = ld4(ch + 1);
                         const uint32_t m = (bm[ch * 4 + (lane >> 3)] >> ((lane & 7) * 4)) & 0xFu;
-                        if (!__any_sync(~0u, m)) continue;
-                        uint32_t tot;
-                        uint32_t r = run + nibble_rank(m, lt, tot);
-                        if (m) {
-                            const uint32_t l0 = ch * 128 + lane * 4;
-                            uint32_t v[4];
-                            // (__ldcg: L2, coherent with this warp's stores before the __syncwarp above,
-                            // and not volatile, so the loads of a step can overlap the log stores)
-                            if (l0 + 4 <= lown) {
-                                const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(out + l0));
-                                v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
-                            } else {
+                        if (__any_sync(~0u, m)) {
+                            uint32_t tot;
+                            uint32_t r = run + nibble_rank(m, lt, tot);
+                            if (m) {
+                                const uint32_t l0 = ch * 128 + lane * 4;
+                                uint32_t v[4] = {q.x, q.y, q.z, q.w};
+                                if (l0 + 4 > lown) {  // the slice's last owned cells
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? (uint32_t)__ldcg(out + l0 + e) : 0u;
-                            }
+                                    for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? (uint32_t)__ldcg(out + l0 + e) : 0u;
+                                }
 #pragma unroll
-                            for (uint32_t e = 0; e < 4; ++e) {
-                                if (!((m >> e) & 1)) continue;
-                                if (p.c.pid16) ent[r] = (l0 + e) | (v[e] << 16);
-                                else reinterpret_cast<uint2 *>(ent)[r] = make_uint2(l0 + e, v[e]);
-                                ++r;
+                                for (uint32_t e = 0; e < 4; ++e) {
+                                    if (!((m >> e) & 1)) continue;
+                                    if (p.c.pid16) ent[r] = (l0 + e) | (v[e] << 16);
+                                    else reinterpret_cast<uint2 *>(ent)[r] = make_uint2(l0 + e, v[e]);
+                                    ++r;
+                                }
                             }
+                            run += tot;
                         }
-                        run += tot;
+                        q = qn;
                     }
                     log_off += rec;
                 } else {  // staging and log are full: spill, emit by re-reading out[] after the prefix
@@ -983,17 +994,39 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             const uint32_t rel = __ldcg(hdr), cnt = __ldcg(hdr + 1);  // this warp's own log (coherent L2 loads)
             const uint32_t *ent = hdr + 4;
             const uint64_t pbase = p.c.pos_base + (s_first + rel) * kSliceT;
+            // 128 entries per step, the next step's loads issued before this one's stores (as in
+            // warp_stream): the replay is a stream, not a chain of load-use latencies
+            const uint32_t steps = (cnt + 127) / 128;
             if (p.c.pid16) {
-#pragma unroll 4
-                for (uint32_t i = lane; i < cnt; i += 32) {
-                    const uint32_t e = __ldcg(ent + i);
-                    put_match(p.c, r0 + i, pbase + (e & 0xFFFFu), e >> 16);
+                uint32_t e[4], en[4];
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) e[k] = lane + 32 * k < cnt ? __ldcg(ent + lane + 32 * k) : 0u;
+                for (uint32_t st = 0; st < steps; ++st) {
+                    const uint32_t i0 = st * 128 + lane;
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k)
+                        en[k] = i0 + 128 + 32 * k < cnt ? __ldcg(ent + i0 + 128 + 32 * k) : 0u;
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k)
+                        if (i0 + 32 * k < cnt) put_match(p.c, r0 + i0 + 32 * k, pbase + (e[k] & 0xFFFFu), e[k] >> 16);
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) e[k] = en[k];
                 }
             } else {
-#pragma unroll 4
-                for (uint32_t i = lane; i < cnt; i += 32) {
-                    const uint2 e = __ldcg(reinterpret_cast<const uint2 *>(ent) + i);
-                    put_match(p.c, r0 + i, pbase + e.x, e.y);
+                const uint2 *ent2 = reinterpret_cast<const uint2 *>(ent);
+                uint2 e[4], en[4];
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) e[k] = lane + 32 * k < cnt ? __ldcg(ent2 + lane + 32 * k) : make_uint2(0, 0);
+                for (uint32_t st = 0; st < steps; ++st) {
+                    const uint32_t i0 = st * 128 + lane;
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k)
+                        en[k] = i0 + 128 + 32 * k < cnt ? __ldcg(ent2 + i0 + 128 + 32 * k) : make_uint2(0, 0);
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k)
+                        if (i0 + 32 * k < cnt) put_match(p.c, r0 + i0 + 32 * k, pbase + e[k].x, e[k].y);
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) e[k] = en[k];
                 }
             }
             r0 += cnt;
