@@ -237,6 +237,31 @@ void derive_host_image(pfac_automaton *a) {
         v = only_child(u, c);
         return (depth[u] + 1 >= Kd) == (depth[u] >= Kd);
     };
+    // The unary run from u: its next L <= maxL forced bases (base i at bits 2i), whether a final state
+    // lies strictly inside (u, u+L), and the state the span ends in.
+    struct Chain {
+        uint64_t bits = 0;
+        uint32_t L = 0, end = 0;
+        bool inner_final = false;
+    };
+    auto chain_of = [&](uint32_t u, uint32_t maxL) {
+        Chain ch;
+        uint32_t v = u, c, w;
+        while (ch.L < maxL && unary_next(v, w)) {
+            if (ch.L > 0 && v >= 1 && v <= a->k) ch.inner_final = true;
+            only_child(v, c);
+            v = w;
+            ch.bits |= (uint64_t)c << (2 * ch.L);
+            ++ch.L;
+        }
+        ch.end = v;
+        return ch;
+    };
+    // uint32 rows: a walk that consumes a span whose end state has no transitions stops there, so
+    // the row can carry that answer (F(end) + 1 in 24 bits; 0 = the end state continues)
+    auto end_answer = [&](const Chain &ch) -> uint32_t {
+        return kEndDead && nchild(ch.end) == 0 && a->F[ch.end] < kEndMask ? a->F[ch.end] + 1 : 0u;
+    };
     std::vector<uint32_t> dev(S, 0);
     uint32_t id = 1;
     auto number_from = [&](std::vector<uint32_t> heads, bool deep) {
@@ -287,25 +312,19 @@ void derive_host_image(pfac_automaton *a) {
         putc(im.F, d, a->F[u]);
         if (kMergedF) putc(im.T, (size_t)d * kRowCells + 4, a->F[u]);  // ablation: F inside the row
         uint32_t v0;
-        if (unary_next(u, v0)) {  // chain row: the next L <= 16 forced bases within u's part
-            uint32_t bits = 0, L = 0, v = u, c, w;
-            bool inner_final = false;  // a final state strictly inside the span (u, u+L)
-            while (L < (uint32_t)kChainMax && unary_next(v, w)) {
-                if (L > 0 && v >= 1 && v <= a->k) inner_final = true;
-                only_child(v, c);
-                v = w;
-                bits |= c << (2 * L);
-                ++L;
-            }
-            const uint32_t nofin = inner_final ? 0u : (cell == 2 ? 0x4000u : 0x40000000u);
-            putc(im.T, (size_t)d * kRowCells + 0, chain_flag | nofin | L);
+        if (unary_next(u, v0)) {  // chain row: the next L forced bases within u's part
+            const Chain ch = chain_of(u, cell == 2 ? (uint32_t)kChainMax : (uint32_t)kChainMax32);
+            const uint32_t nofin = ch.inner_final ? 0u : (cell == 2 ? 0x4000u : 0x40000000u);
             if (cell == 2) {
-                putc(im.T, (size_t)d * kRowCells + 1, bits & 0xFFFFu);
-                putc(im.T, (size_t)d * kRowCells + 2, bits >> 16);
+                putc(im.T, (size_t)d * kRowCells + 0, chain_flag | nofin | ch.L);
+                putc(im.T, (size_t)d * kRowCells + 1, (uint32_t)ch.bits & 0xFFFFu);
+                putc(im.T, (size_t)d * kRowCells + 2, (uint32_t)ch.bits >> 16);
                 putc(im.T, (size_t)d * kRowCells + 3, a->F[u]);
             } else {
-                putc(im.T, (size_t)d * kRowCells + 1, bits);
+                putc(im.T, (size_t)d * kRowCells + 0, chain_flag | nofin | (end_answer(ch) << kEndShift) | ch.L);
+                putc(im.T, (size_t)d * kRowCells + 1, (uint32_t)ch.bits);
                 putc(im.T, (size_t)d * kRowCells + 2, a->F[u]);
+                putc(im.T, (size_t)d * kRowCells + 3, (uint32_t)(ch.bits >> 32));
             }
         } else {
             for (int c = 0; c < 4; ++c)
@@ -345,6 +364,8 @@ void derive_host_image(pfac_automaton *a) {
         // J2 entry becomes ALIVE | HRF | index.  Branch heads keep pointing into T.
         im.HR.clear();
         im.hr_nb = 0;
+        std::vector<uint32_t> canon(cell == 4 ? (size_t)S + 1 : 0, 0);  // device id -> canonical id
+        for (uint32_t u = 0; cell == 4 && u < S; ++u) canon[dev[u]] = u;
         if (cell == 4 && im.S < (1u << 30)) {
             uint64_t heads = 0;
             for (uint64_t x = 0; x < n2; ++x)
@@ -356,6 +377,10 @@ void derive_host_image(pfac_automaton *a) {
                     uint32_t row[4];
                     memcpy(row, im.T.data() + (size_t)s * kRowCells * 4, 16);
                     if (!(row[0] & 0x80000000u)) continue;  // a branch row: stays in T
+                    // the copy spans at most 16 bases (cell 3 holds the head's device id)
+                    const Chain ch = chain_of(canon[s], (uint32_t)kChainMax);
+                    row[0] = 0x80000000u | (ch.inner_final ? 0u : 0x40000000u) | (end_answer(ch) << kEndShift) | ch.L;
+                    row[1] = (uint32_t)ch.bits;
                     row[3] = s;
                     const uint32_t h = (uint32_t)(im.HR.size() / 4);
                     im.HR.insert(im.HR.end(), row, row + 4);
@@ -364,7 +389,7 @@ void derive_host_image(pfac_automaton *a) {
                     // first 4 forced bases; a walk whose next 4 bases differ (or that has fewer than
                     // 4 left) ends inside the span and answers 0 without loading the row (all but
                     // ~1/256 of the live walks on random text).
-                    const bool nb = (row[0] & 0x40000000u) && (row[0] & 31u) >= kHRBases && row[2] == 0 &&
+                    const bool nb = (row[0] & 0x40000000u) && (row[0] & kChainLenMask32) >= kHRBases && row[2] == 0 &&
                                     h < (1u << kHRIndexBitsNB);
                     im.hr_nb += nb ? 1u : 0u;
                     im.J2[x] = nb ? kJ2Alive | kJ2HR | kJ2NB | ((row[1] & 0xFFu) << kHRIndexBitsNB) | h

@@ -111,9 +111,11 @@ struct Row<uint32_t> {
     uint32_t f;  // PFAC_MERGED_F: F(s) from the row's cell 4
     __device__ __forceinline__ bool chain() const { return r.x & 0x80000000u; }
     __device__ __forceinline__ bool nofin() const { return r.x & 0x40000000u; }
-    __device__ __forceinline__ uint32_t len() const { return r.x & 31u; }
+    __device__ __forceinline__ uint32_t len() const { return r.x & kChainLenMask32; }
     __device__ __forceinline__ uint32_t bits() const { return r.y; }
+    __device__ __forceinline__ uint64_t bits64() const { return ((uint64_t)r.w << 32) | r.y; }  // T rows only
     __device__ __forceinline__ uint32_t fin() const { return r.z; }
+    __device__ __forceinline__ uint32_t end_answer() const { return (r.x >> kEndShift) & kEndMask; }  // F(end) + 1
     __device__ __forceinline__ uint32_t child(uint32_t c) const {
         return c & 2 ? (c & 1 ? r.w : r.z) : (c & 1 ? r.y : r.x);
     }
@@ -209,20 +211,38 @@ __device__ __forceinline__ uint32_t window16(const uint32_t *txt, uint32_t l) {
     return (uint32_t)(((((uint64_t)txt[q + 1]) << 32) | txt[q]) >> ((l & 15) * 2));
 }
 
+// 32 bases starting at local offset l (base i in bits 2i).
+__device__ __forceinline__ uint64_t window32(const uint32_t *txt, uint32_t l) {
+    const uint32_t q = l >> 4, sh = (l & 15) * 2;
+    const uint32_t a = txt[q], b = txt[q + 1], c = txt[q + 2];
+    return ((uint64_t)__funnelshift_r(b, c, sh) << 32) | __funnelshift_r(a, b, sh);
+}
+
 // The PFAC walk from state s reading bases l, l+1, ... (< lend): follow the goto function until the
-// first missing transition.  A chain row advances over up to 16 forced bases with
-// one XOR; the answer is F of the last state reached (the deepest final passed).  A walk that ends
-// inside a NOFIN chain span returns the row's own F without another lookup.
+// first missing transition.  A chain row advances over its forced bases with one
+// XOR (up to 16 per uint16 row, 32 per uint32 row); the answer is F of the last state reached (the
+// deepest final passed).  A walk that ends inside a NOFIN chain span returns the row's own F without
+// another lookup; one that consumes a uint32 span ending in a state without transitions returns the
+// row's end answer.
 template <typename CT, bool WIN>
 __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t *txt, uint32_t s, uint32_t l,
                                          uint32_t lend) {
     while (l < lend) {
-        const uint32_t w = window16(txt, l);
         const Row<CT> r = tb.row(s);
+        uint32_t m, c0;
+        if constexpr (sizeof(CT) == 4) {
+            const uint64_t w = window32(txt, l);
+            const uint64_t d = w ^ r.bits64();
+            m = d ? (uint32_t)(__ffsll((long long)d) - 1) >> 1 : 32u;  // matching leading bases
+            c0 = (uint32_t)w & 3u;
+        } else {
+            const uint32_t w = window16(txt, l);
+            const uint32_t d = w ^ r.bits();
+            m = d ? (uint32_t)(__ffs(d) - 1) >> 1 : 16u;
+            c0 = w & 3u;
+        }
         if (r.chain()) {
             const uint32_t L = r.len();
-            const uint32_t d = w ^ r.bits();
-            const uint32_t m = d ? (uint32_t)(__ffs(d) - 1) >> 1 : 16u;  // matching leading bases
             const uint32_t rem = lend - l;
             const uint32_t lim = L < rem ? L : rem;
             if (m < lim || lim < L) {  // the walk ends inside this span, at s + min(m, lim)
@@ -231,10 +251,13 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
                 s += mm;
                 break;
             }
+            if constexpr (sizeof(CT) == 4) {
+                if (const uint32_t e = r.end_answer()) return e - 1;  // the span ends in a dead end
+            }
             s += L;
             l += L;
         } else {
-            const uint32_t t = r.child(w & 3u);
+            const uint32_t t = r.child(c0);
             if (!t) {
                 if constexpr (kMergedF) return r.f;  // the answer came with the row
                 break;
@@ -266,6 +289,7 @@ __device__ __forceinline__ uint32_t walk_head(const Tab<CT, WIN> &tb, const uint
         if (r.nofin() || mm == 0) return r.fin();
         return tb.final_of(s + mm);
     }
+    if (const uint32_t e = r.end_answer()) return e - 1;  // the span ends in a dead end
     return walk(tb, txt, s + L, l + L, lend);
 }
 
@@ -647,20 +671,27 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
         // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
         auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3) {
-            // The lanes' slots are the exclusive prefix of their counts c, from ballots of the bits of c
-            // (independent instructions, no shuffle chain): two when every c <= 3 (sparse groups),
-            // six otherwise (c <= 32).  Each lane then writes its own positions -- no ballot round
-            // per queued position.
+            // The lanes' slots are the exclusive prefix of their counts c: from two ballots of the bits
+            // of c when every c <= 3 (sparse groups: no shuffle chain), else a shuffle scan.  Each lane
+            // then writes its own positions -- no ballot round per queued position.
             const uint32_t c = __popc(am);
             uint32_t excl = 0, total = 0;
             if (kPushScan) {
-                const uint32_t nb = __ballot_sync(~0u, c > 3) ? 6 : 2;
-                for (uint32_t k = 0; k < nb; ++k) {
-                    const uint32_t b = __ballot_sync(~0u, (c >> k) & 1u);
-                    excl += __popc(b & lt) << k;
-                    total += __popc(b) << k;
+                if (!__ballot_sync(~0u, c > 3)) {
+                    const uint32_t b0 = __ballot_sync(~0u, c & 1u), b1 = __ballot_sync(~0u, c & 2u);
+                    excl = __popc(b0 & lt) + 2 * __popc(b1 & lt);
+                    total = __popc(b0) + 2 * __popc(b1);
+                    if (total == 0) return;
+                } else {
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(~0u, incl, d);
+                        if (lane >= (uint32_t)d) incl += y;
+                    }
+                    excl = incl - c;
+                    total = __shfl_sync(~0u, incl, 31);
                 }
-                if (total == 0) return;
             }
             if (kPushScan && qn + total <= kQCap) {  // the group fits: each lane writes its own
                 uint32_t slot = qn + excl;

@@ -33,7 +33,18 @@ constexpr int kK2Max = PFAC_K2MAX;  // largest second-level jump length (4^11 ce
 #define PFAC_K2MIN PFAC_FBK
 #endif
 constexpr int kK2Min = PFAC_K2MIN;  // smallest (>= kFilterK: the filter must not look further than J2)
-constexpr int kChainMax = 16; // bases per chain row (2 bits each -> one 32-bit word)
+constexpr int kChainMax = 16; // bases per uint16 chain row (2 bits each -> one 32-bit word)
+// uint32 chain rows: up to 32 forced bases (cells 1 and 3), and the answer of a walk that consumes the
+// whole span when the span's end state has no transitions (cell 0 bits 6-29: F(end) + 1, 0 = none)
+#ifndef PFAC_CHAIN32
+#define PFAC_CHAIN32 1  // A/B knob: 0 = 16 bases per uint32 chain row
+#endif
+constexpr int kChainMax32 = PFAC_CHAIN32 ? 32 : 16;
+#ifndef PFAC_ENDDEAD
+#define PFAC_ENDDEAD 1  // A/B knob: 0 = no end-state answers in uint32 chain rows
+#endif
+constexpr bool kEndDead = PFAC_ENDDEAD;
+constexpr uint32_t kChainLenMask32 = 63u, kEndShift = 6, kEndMask = 0xFFFFFFu;
 // Ablation (the paper's "two arrays vs one merged array"): PFAC_MERGED_F=1
 // stores F(s) in cell 4 of an 8-cell row next to the 4 transitions, so a walk that ends at a branch
 // state reads its answer from the row it already holds (rows twice as wide).  Default: T rows of 4
