@@ -324,6 +324,8 @@ def run_pfac(args):
     t0 = time.perf_counter()
     a = P.Automaton(pats)
     build_ms = (time.perf_counter() - t0) * 1e3
+    if args.text_kernel is not None:
+        a.set_text_kernel(args.text_kernel)
     t0 = time.perf_counter()
     a.prepare(local)
     prepare_ms = (time.perf_counter() - t0) * 1e3
@@ -656,6 +658,8 @@ def main():
                     help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")
     ap.add_argument("--all-matches", action="store_true",
                     help="add the all-occurrence expansion (pfac_expand_async) to the timed step")
+    ap.add_argument("--text-kernel", type=int, default=None, choices=[-1, 0, 1, 2],
+                    help="pfac_set_text_kernel mode for the text path (default: the library's plan)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -224,6 +224,14 @@ uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int l
  * are identical in every mode; only the kernels differ.  PFAC_E_ARG for other modes or a null a.
  * The one mutable property of an automaton (an atomic; safe to change between calls). */
 int pfac_set_text_kernel(pfac_automaton *a, int mode);
+/* A cheap statistic of a text for that policy (host memory, host code, no device work): the PFAC
+ * walk (goto function only; a byte outside ACGTacgt has no transition, reading R5)
+ * from positions 0, stride, 2*stride, ... < n of h_text, counting transitions.  *deep_frac = share
+ * of the sampled walks with >= deep transitions, *mean_steps = mean transitions per sampled walk.
+ * Repetitive text against nested patterns (long walks) shows a large deep_frac; random text a tiny
+ * one.  PFAC_E_ARG for null pointers (h_text may be null when n = 0) or stride = 0. */
+int pfac_text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_t n, uint64_t stride,
+                         uint32_t deep, double *deep_frac, double *mean_steps);
 int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64_t n_own, uint64_t n_avail,
                           int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                           uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad,

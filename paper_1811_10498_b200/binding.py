@@ -41,6 +41,9 @@ _SIGS = {
     "pfac_match_packed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_set_text_kernel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "pfac_text_walk_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.c_uint32, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_double)]),
     "pfac_compact_workspace_bytes": (ctypes.c_uint64, [ctypes.c_uint64]),
     "pfac_compact_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32,
@@ -151,6 +154,14 @@ def _flatten(patterns) -> tuple[np.ndarray, np.ndarray]:
     return data, offs
 
 
+def _host_bytes(text) -> np.ndarray:
+    if isinstance(text, (bytes, bytearray)):
+        return np.frombuffer(bytes(text), np.uint8)
+    if hasattr(text, "numpy"):  # a CPU torch tensor
+        return text.numpy().view(np.uint8).reshape(-1)
+    return np.asarray(text, dtype=np.uint8).reshape(-1)
+
+
 # pfac_set_text_kernel mode applied to every new Automaton when its text_kernel argument is None
 # (None: the library's default, the plan's choice).  Tests switch it to cover every text path.
 DEFAULT_TEXT_KERNEL = None
@@ -173,6 +184,15 @@ class Automaton:
     def set_text_kernel(self, mode: int) -> None:
         """pfac_set_text_kernel: the path policy of match_text_async for this automaton."""
         _check(lib().pfac_set_text_kernel(self._h, int(mode)))
+
+    def text_walk_stats(self, text, stride: int = 1, deep: int = 16) -> tuple[float, float]:
+        """pfac_text_walk_stats on a host text (numpy uint8 / bytes / CPU tensor): (deep_frac,
+        mean_steps) of the walks from every stride-th position."""
+        t = np.ascontiguousarray(_host_bytes(text))
+        df, ms = ctypes.c_double(), ctypes.c_double()
+        _check(lib().pfac_text_walk_stats(self._h, t.ctypes.data if len(t) else None, len(t), int(stride), int(deep),
+                                          ctypes.byref(df), ctypes.byref(ms)))
+        return df.value, ms.value
 
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:

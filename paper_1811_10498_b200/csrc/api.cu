@@ -336,6 +336,11 @@ int pfac_set_text_kernel(pfac_automaton *a, int mode) {
     return PFAC_OK;
 }
 
+int pfac_text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_t n, uint64_t stride, uint32_t deep,
+                         double *deep_frac, double *mean_steps) {
+    return text_walk_stats(a, h_text, n, stride, deep, deep_frac, mean_steps);
+}
+
 uint64_t pfac_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
 
 int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv,

@@ -414,4 +414,31 @@ void derive_host_image(pfac_automaton *a) {
     }
 }
 
+// Walk statistics of a host text sample (pfac_text_walk_stats): the PFAC walk from
+// positions 0, stride, 2*stride, ... over the canonical table, counting transitions; a byte outside
+// ACGTacgt has no transition (reading R5).  Host code only.
+int text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_t n, uint64_t stride, uint32_t deep,
+                    double *deep_frac, double *mean_steps) {
+    if (!a || (!h_text && n) || !stride || !deep_frac || !mean_steps)
+        return fail(PFAC_E_ARG, "pfac_text_walk_stats: null argument or zero stride");
+    uint64_t walks = 0, deep_walks = 0, steps = 0;
+    for (uint64_t i = 0; i < n; i += stride) {
+        uint32_t s = 0, d = 0;
+        for (uint64_t j = i; j < n; ++j) {
+            const int c = base_code(h_text[j]);
+            if (c < 0) break;
+            const uint32_t t = a->table[(size_t)s * 4 + c];
+            if (!t) break;
+            s = t;
+            ++d;
+        }
+        ++walks;
+        steps += d;
+        deep_walks += d >= deep;
+    }
+    *deep_frac = walks ? (double)deep_walks / (double)walks : 0.0;
+    *mean_steps = walks ? (double)steps / (double)walks : 0.0;
+    return PFAC_OK;
+}
+
 }  // namespace pfac

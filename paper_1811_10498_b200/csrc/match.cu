@@ -1168,7 +1168,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     pl.slice_words_1k = kSliceSmall / 16 + halo_words_for(h.K2 > h.K ? h.K2 : h.K, maxlen);
     const size_t fixed_k = match_smem(table, pl.cell, 0, pl.slice_words_1k, true, true, kSliceSmall / 32) +
                            kStaticSmemReserve;
-    pl.txt1k_ok = h.K2 != 0 && pl.cell == 4 && (size_t)optin >= fixed_k;
+    pl.txt1k_ok = h.K2 != 0 && (size_t)optin >= fixed_k;
     uint32_t wk = pl.txt1k_ok ? (uint32_t)(((size_t)optin - fixed_k) / (kWinCells * pl.cell)) & ~7u : 0u;
     if (wk < h.rows && (uint64_t)h.rows > (uint64_t)kWindowMinShare * wk) wk = 0;
 #ifdef PFAC_WINDOW_MAX
@@ -1222,9 +1222,13 @@ static const void *kernel_for(const DeviceImage &img, bool bar, bool list = fals
                               bool small = false) {
     const MatchPlan &pl = img.plan;
     if constexpr (FUSE) {
-        if (txt && small)  // text input, 1024-position slices (uint32 images only)
+        if (txt && small) {  // text input, 1024-position slices
+            if (pl.cell == 2)
+                return list ? txt_kernel<uint16_t, true, kSliceSmall>(pl.all_smem_txt1k)
+                            : txt_kernel<uint16_t, false, kSliceSmall>(pl.all_smem_txt1k);
             return list ? txt_kernel<uint32_t, true, kSliceSmall>(pl.all_smem_txt1k)
                         : txt_kernel<uint32_t, false, kSliceSmall>(pl.all_smem_txt1k);
+        }
         if (txt) {  // text input (filter path; checked by the launcher)
             if (pl.cell == 2) return list ? txt_kernel<uint16_t, true>(pl.all_smem_txt) : txt_kernel<uint16_t, false>(pl.all_smem_txt);
             return list ? txt_kernel<uint32_t, true>(pl.all_smem_txt) : txt_kernel<uint32_t, false>(pl.all_smem_txt);

@@ -175,6 +175,8 @@ int fail(int code, const std::string &msg);
 // builder.cpp
 int build_automaton(const uint8_t *bytes, const uint64_t *offsets, uint32_t k, pfac_automaton **out);
 void derive_host_image(pfac_automaton *a);
+int text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_t n, uint64_t stride, uint32_t deep,
+                    double *deep_frac, double *mean_steps);
 
 // kernels.cu launchers (all asynchronous on `stream`); return cudaError_t as int.
 int launch_pack(const uint8_t *d_text, uint64_t n, uint32_t *d_packed, uint64_t nwords_padded,

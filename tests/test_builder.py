@@ -165,3 +165,34 @@ def test_prefix_chain_definition():
             pre = [j for j, q in enumerate(pats, start=1) if len(q) < len(p) and p.startswith(q)]
             parent = max(pre, key=lambda j: len(pats[j - 1])) if pre else 0
             assert ch[i].tolist() == [parent, len(pre) + 1], (p, pats)
+
+
+def test_text_walk_stats_closed_forms():
+    """pfac_text_walk_stats (host code): transition counts of the PFAC walk from
+    sampled positions, against closed forms.  All 4^3 3-mers: every walk makes min(3, n - i)
+    transitions.  Nested family A^1..A^10 over A^25 C A^5 N A^4: min(10, run left) inside A runs,
+    0 at C and at the N barrier (reading R5)."""
+    rng = np.random.default_rng(5)
+    a = Automaton(gen.all_kmers(3))
+    n = 1000
+    text = rng.choice(np.frombuffer(b"ACGT", np.uint8), n)
+    steps = [min(3, n - i) for i in range(n)]
+    for stride in (1, 7):
+        s = steps[::stride]
+        df, ms = a.text_walk_stats(text, stride=stride, deep=3)
+        assert df == pytest.approx(sum(x >= 3 for x in s) / len(s)) and ms == pytest.approx(sum(s) / len(s))
+    b = Automaton([b"A" * m for m in range(1, 11)])
+    t = b"A" * 25 + b"C" + b"A" * 5 + b"N" + b"aaaa"  # lowercase: the same bases (reading R4)
+    run_left = []
+    for i, ch in enumerate(t):
+        j = i
+        while j < len(t) and t[j] in b"Aa":
+            j += 1
+        run_left.append(min(10, j - i))
+    for deep in (1, 5, 10):
+        df, ms = b.text_walk_stats(t, deep=deep)
+        assert df == pytest.approx(sum(x >= deep for x in run_left) / len(t))
+        assert ms == pytest.approx(sum(run_left) / len(t))
+    assert b.text_walk_stats(b"", deep=4) == (0.0, 0.0)
+    with pytest.raises(PfacError):
+        b.text_walk_stats(t, stride=0)

@@ -31,7 +31,7 @@ U64MAX = (1 << 64) - 1
 def text_kernel(request, monkeypatch):
     """Both paths of pfac_match_text_async: the one-kernel TXT instantiation and the pack + fused
     kernel path the call takes for unaligned text or automata the policy keeps off TXT; "2": the text
-    kernel with 1024-position slices (uint32 images; uint16 ones take the two-kernel path)."""
+    kernel with 1024-position slices (both cell widths)."""
     monkeypatch.setattr(P.binding, "DEFAULT_TEXT_KERNEL", int(request.param))
     return request.param
 
@@ -187,7 +187,7 @@ def test_text_policy_info(text_kernel):
     """The image reports which path the call takes (pfac_image_info.text_kernel)."""
     a = P.Automaton(SETS["cfg2like"]())
     info = a.image_info(0)
-    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 0}[text_kernel]  # uint16 image
+    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 2}[text_kernel]  # uint16 image
     b = P.Automaton(SETS["big32"]())  # uint32 image
     assert b.image_info(0)["text_kernel"] == {"1": 1, "0": 0, "2": 2}[text_kernel]
     b.set_text_kernel(-1)  # back to the plan: a uint32 image with < 2^20 rows takes 2048-slice text
