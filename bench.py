@@ -324,8 +324,14 @@ def run_pfac(args):
     t0 = time.perf_counter()
     a = P.Automaton(pats)
     build_ms = (time.perf_counter() - t0) * 1e3
+    text_plan = None
     if args.text_kernel is not None:
         a.set_text_kernel(args.text_kernel)
+    else:  # the library's text plan from a host sample of this rank's text (outside the timed region)
+        stride = max(1, len(text) // 200_000)
+        mode, deep = a.plan_text(text, stride=stride)
+        text_plan = {"api": "pfac_plan_text", "sample_positions": -(-len(text) // stride),
+                     "deep_walk_share": deep, "mode": mode}
     t0 = time.perf_counter()
     a.prepare(local)
     prepare_ms = (time.perf_counter() - t0) * 1e3
@@ -599,7 +605,8 @@ def run_pfac(args):
                        **({"ranks_per_gpu": -(-world // ndev), "backend": args.backend} if world > 1 else {}),
                        **({"gather_check": gather_check} if gather_check else {}),
                        "l2": "inputs larger than L2 (no flush): ASCII text 1 B/base, out[] 4 B/base",
-                       "matches_per_step": m_final, "image": a.image_info(local)},
+                       "matches_per_step": m_final, "image": a.image_info(local),
+                       **({"text_plan": text_plan} if text_plan else {})},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
                          "kernel": ("match_kernel<TXT=1" + (", 1024-position slices" if text_variant == 2 else "") +

@@ -232,6 +232,16 @@ int pfac_set_text_kernel(pfac_automaton *a, int mode);
  * one.  PFAC_E_ARG for null pointers (h_text may be null when n = 0) or stride = 0. */
 int pfac_text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_t n, uint64_t stride,
                          uint32_t deep, double *deep_frac, double *mean_steps);
+/* The text-call path from a text sample (host memory; host code, no device work): the walk statistic
+ * above (deep = 16, every stride-th position) decides -- walk-heavy text (>= 1% of the sampled walks
+ * make 16 or more transitions: repetitive text against nested patterns) takes the 1024-position-slice
+ * text kernel (mode 2), whose smaller per-warp staging leaves shared memory for a row window and L1
+ * room for rows (measured on cfg5: 3.61 ms vs 3.96 ms with 2048-position slices and 3.69 ms for pack +
+ * fused); other text keeps the automaton's plan (mode -1).  Applies the mode with
+ * pfac_set_text_kernel and returns it in *mode (nullable), the statistic in *deep_frac (nullable).
+ * Errors as pfac_text_walk_stats. */
+int pfac_plan_text(pfac_automaton *a, const uint8_t *h_sample, uint64_t n, uint64_t stride, int *mode,
+                   double *deep_frac);
 int pfac_match_text_async(const pfac_automaton *a, const uint8_t *d_text, uint64_t n_own, uint64_t n_avail,
                           int32_t *d_out, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                           uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, uint64_t *d_first_bad,

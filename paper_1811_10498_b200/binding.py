@@ -41,6 +41,8 @@ _SIGS = {
     "pfac_match_packed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_set_text_kernel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "pfac_plan_text": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]),
     "pfac_text_walk_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint32, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_double)]),
@@ -193,6 +195,14 @@ class Automaton:
         _check(lib().pfac_text_walk_stats(self._h, t.ctypes.data if len(t) else None, len(t), int(stride), int(deep),
                                           ctypes.byref(df), ctypes.byref(ms)))
         return df.value, ms.value
+
+    def plan_text(self, sample, stride: int = 1) -> tuple[int, float]:
+        """pfac_plan_text: set the text-call path from a host text sample; returns (mode, deep_frac)."""
+        t = np.ascontiguousarray(_host_bytes(sample))
+        m, df = ctypes.c_int(), ctypes.c_double()
+        _check(lib().pfac_plan_text(self._h, t.ctypes.data if len(t) else None, len(t), int(stride),
+                                    ctypes.byref(m), ctypes.byref(df)))
+        return m.value, df.value
 
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:

@@ -341,6 +341,21 @@ int pfac_text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_
     return text_walk_stats(a, h_text, n, stride, deep, deep_frac, mean_steps);
 }
 
+constexpr uint32_t kDeepWalk = 16;       // pfac_plan_text: a walk of >= 16 transitions is "deep"
+constexpr double kWalkHeavyShare = 0.01;  // ... and >= 1% deep walks make a text walk-heavy (cfg5: 21%, cfg2-4 < 0.04%)
+
+int pfac_plan_text(pfac_automaton *a, const uint8_t *h_sample, uint64_t n, uint64_t stride, int *mode,
+                   double *deep_frac) {
+    double df = 0, ms = 0;
+    const int rc = text_walk_stats(a, h_sample, n, stride, kDeepWalk, &df, &ms);
+    if (rc != PFAC_OK) return rc;
+    const int m = df >= kWalkHeavyShare ? 2 : -1;
+    a->text_kernel.store(m, std::memory_order_relaxed);
+    if (mode) *mode = m;
+    if (deep_frac) *deep_frac = df;
+    return PFAC_OK;
+}
+
 uint64_t pfac_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
 
 int pfac_match_compact_barriers_async(const pfac_automaton *a, const uint32_t *d_packed, const uint16_t *d_inv,

@@ -21,7 +21,9 @@ VARIANTS = {
     "nolog": ["PFAC_MATCH_LOG=0"],           # A/B: no match log (dense matches spill to the out[] re-read)
     "nolog_ballot": ["PFAC_MATCH_LOG=0", "PFAC_PUSH_SCAN=0"],
     "ipl2": ["PFAC_DRAIN_IPL=2"],            # A/B: two queued positions per lane per drain round (2048-position slices too)
-    "ipl1": ["PFAC_DRAIN_IPL_1K=1"],         # A/B: one per lane in the 1024-position-slice kernels too
+    "ipl1": ["PFAC_DRAIN_IPL_1K=1"],
+    "ipl3": ["PFAC_DRAIN_IPL_1K=3"],
+    "ipl4": ["PFAC_DRAIN_IPL_1K=4"],         # A/B: one per lane in the 1024-position-slice kernels too
     "chain16": ["PFAC_CHAIN32=0"],           # A/B: 16 forced bases per uint32 chain row (round 1)
     "noend": ["PFAC_ENDDEAD=0"],             # A/B: no end-state answers in uint32 chain rows
     "fb_add": ["PFAC_FB_LOP=0"],             # A/B: filter word addresses as base + offset (one more IADD per lookup)
