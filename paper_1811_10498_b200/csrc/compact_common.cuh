@@ -60,20 +60,21 @@ __device__ __forceinline__ uint64_t warp_stream(const CompactArgs &a, uint64_t l
     const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1;
     uint64_t local = 0;
     uint4 v[4], vn[4];
-    if (lo < hi) load_step<NC>(a.out, a.n, lo, lane, v);
+    if (lo < hi && !bits) load_step<NC>(a.out, a.n, lo, lane, v);
     for (uint64_t b = lo; b < hi; b += kStep) {
-        if (b + kStep < hi) load_step<NC>(a.out, a.n, b + kStep, lane, vn);
-        if (bits) {  // lane's 4 positions b + 128q + 4 lane .. +3: a nibble of word (b + 128q)/32 + lane/8
+        if (b + kStep < hi && !bits) load_step<NC>(a.out, a.n, b + kStep, lane, vn);
+        if (bits) {  // lane's 4 positions b + 128q + 4 lane .. +3: a nibble of word (b + 128q)/32 + lane/8;
+                     // only the cells whose bit is set are read (the others were never written)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint64_t p0 = b + 128 * q + 4 * lane;
                 const uint32_t m = p0 < hi ? (ld_cg_u32(reinterpret_cast<const int32_t *>(bits + (p0 >> 5))) >>
                                               (p0 & 31)) & 0xFu
                                            : 0u;
-                v[q].x = m & 1 ? v[q].x : 0u;
-                v[q].y = m & 2 ? v[q].y : 0u;
-                v[q].z = m & 4 ? v[q].z : 0u;
-                v[q].w = m & 8 ? v[q].w : 0u;
+                v[q].x = m & 1 ? ld_cg_u32(a.out + p0) : 0u;
+                v[q].y = m & 2 ? ld_cg_u32(a.out + p0 + 1) : 0u;
+                v[q].z = m & 4 ? ld_cg_u32(a.out + p0 + 2) : 0u;
+                v[q].w = m & 8 ? ld_cg_u32(a.out + p0 + 3) : 0u;
             }
         }
         uint32_t any = 0;

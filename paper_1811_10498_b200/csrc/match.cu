@@ -330,6 +330,10 @@ static __host__ __device__ constexpr uint32_t qcap_for(uint32_t bm_words) {
 #define PFAC_PUSH_SCAN 1  // A/B knob: 0 = one ballot round per queued position per lane
 #endif
 constexpr bool kPushScan = PFAC_PUSH_SCAN;
+#ifndef PFAC_DEFER
+#define PFAC_DEFER 1  // A/B knob: 0 = every group's queue drained before the next group's filter step
+#endif
+constexpr bool kDeferRound = PFAC_DEFER;
 #ifndef PFAC_MATCH_LOG
 #define PFAC_MATCH_LOG 1  // A/B knob: 0 = no per-warp match log (a full staging area spills at once)
 #endif
@@ -611,48 +615,55 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         uint32_t qn = 0;  // warp-uniform length of the queue of alive positions
         // Walk the queued positions 32 at a time (one per lane) until at most `keep` remain.  The
         // __syncwarp orders the queue writes and the owners' v4 stores before these patch stores.
+        // A drain round: issue() takes up to 32 * kDrainIPL queued items (kDrainIPL per lane) and issues
+        // all their J2 loads; resolve() consumes them (an NB check, a chain-head row, a walk) and
+        // patches out[].  One L2 round trip serves the whole round.
+        uint32_t dl[kDrainIPL], dg[kDrainIPL], dle[kDrainIPL];  // position, J2 entry, walk bound (barrier)
+        auto issue = [&](uint32_t take, uint32_t qb) {
+#pragma unroll
+            for (uint32_t k = 0; k < kDrainIPL; ++k) {
+                const uint32_t i = lane + 32 * k;
+                dl[k] = i < take ? queue[qb + i] : 0xFFFFu;
+                dle[k] = (BAR && bar_slice && i < take) ? next_barrier(dl[k]) : lend;
+                dg[k] = (i < take && dl[k] + p.K2 <= dle[k]) ? ld_tab(p.J2 + (window16(txt, dl[k]) & p.mask2))
+                                                             : 0xFFFFFFFFu;
+            }
+        };
+        auto resolve = [&]() {
+#pragma unroll
+            for (uint32_t k = 0; k < kDrainIPL; ++k) {
+                const uint32_t l = dl[k], g = dg[k], le = dle[k];
+                if (l == 0xFFFFu) continue;
+                uint32_t res;
+                if (g == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l, le);  // near the end / a barrier
+                else if (sizeof(CT) == 4 && p.HR && (g & kJ2HR)) {  // a chain head's row copy
+                    // NB entry: unless the next 4 bases are the chain's first 4 (and readable), the walk
+                    // ends inside the NOFIN span of an F = 0 head: the answer is 0 without the row load
+                    // (builder.cpp, pfac_internal.h)
+                    const uint32_t l2 = l + p.K2;
+                    if ((g & kJ2NB) && (le - l2 < kHRBases || ((window16(txt, l2) ^ (g >> kHRIndexBitsNB)) & 0xFFu)))
+                        res = 0;
+                    else
+                        res = walk_head(tb, txt, ld_tab(p.HR + (g & (g & kJ2NB ? (1u << kHRIndexBitsNB) - 1 : kJ2NB - 1))),
+                                        l2, le);
+                }
+                else if (g & 0x80000000u) res = walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, le);
+                else res = g;
+                if (!LIST || res) out[l] = (int32_t)res;
+                if (FUSE && res) atomicOr(&bm[l >> 5], 1u << (l & 31));
+            }
+        };
+        bool pending = false;  // a round issued at the end of one group and resolved after the next one's filter
+        // Walk the queued positions (FBM: rounds as above) until at most `keep` remain.  The
+        // __syncwarp orders the queue writes and the owners' v4 stores before these patch stores.
         auto drain = [&](uint32_t keep) {
             while (qn > keep) {
                 __syncwarp();
                 if constexpr (FBM) {
-                    // up to kDrainIPL items per lane per round: all their J2 loads are issued before any is
-                    // consumed, so one L2 round trip serves up to 32 * kDrainIPL positions
                     const uint32_t avail = qn - keep;
                     const uint32_t take = avail < 32 * kDrainIPL ? avail : 32 * kDrainIPL;
-                    const uint32_t qb = qn - take;
-                    uint32_t l[kDrainIPL], g[kDrainIPL], le[kDrainIPL];  // le: walk bound (barrier)
-#pragma unroll
-                    for (uint32_t k = 0; k < kDrainIPL; ++k) {
-                        const uint32_t i = lane + 32 * k;
-                        l[k] = i < take ? queue[qb + i] : 0xFFFFu;
-                        le[k] = (BAR && bar_slice && i < take) ? next_barrier(l[k]) : lend;
-                        g[k] = (i < take && l[k] + p.K2 <= le[k]) ? ld_tab(p.J2 + (window16(txt, l[k]) & p.mask2))
-                                                                   : 0xFFFFFFFFu;
-                    }
-#pragma unroll
-                    for (uint32_t k = 0; k < kDrainIPL; ++k) {
-                        if (l[k] == 0xFFFFu) continue;
-                        uint32_t res;
-                        if (g[k] == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l[k], le[k]);  // near the end / a barrier
-                        else if (sizeof(CT) == 4 && p.HR && (g[k] & kJ2HR)) {  // a chain head's row copy
-                            // NB entry: unless the next 4 bases are the chain's first 4 (and readable),
-                            // the walk ends inside the NOFIN span of an F = 0 head: the answer is 0
-                            // without the row load (builder.cpp, pfac_internal.h)
-                            const uint32_t l2 = l[k] + p.K2;
-                            if ((g[k] & kJ2NB) && (le[k] - l2 < kHRBases ||
-                                                   ((window16(txt, l2) ^ (g[k] >> kHRIndexBitsNB)) & 0xFFu)))
-                                res = 0;
-                            else
-                                res = walk_head(tb, txt,
-                                                ld_tab(p.HR + (g[k] & (g[k] & kJ2NB ? (1u << kHRIndexBitsNB) - 1
-                                                                                   : kJ2NB - 1))),
-                                                l2, le[k]);
-                        }
-                        else if (g[k] & 0x80000000u) res = walk(tb, txt, g[k] & 0x7FFFFFFFu, l[k] + p.K2, le[k]);
-                        else res = g[k];
-                        if (!LIST || res) out[l[k]] = (int32_t)res;
-                        if (FUSE && res) atomicOr(&bm[l[k] >> 5], 1u << (l[k] & 31));
-                    }
+                    issue(take, qn - take);
+                    resolve();
                     qn -= take;
                 } else {
                     const uint32_t take = qn - keep < 32 ? qn - keep : 32;
@@ -667,10 +678,31 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 __syncwarp();
             }
         };
+        // the end of a group: drain to at most one round; with `defer`, issue that round's loads and leave
+        // it pending (resolved after the next group's filter step, which hides the L2 latency)
+        auto finish = [&](bool defer) {
+            if (kDeferRound && FBM && defer) {
+                drain(32 * kDrainIPL);
+                if (qn) {
+                    __syncwarp();
+                    issue(qn, 0);
+                    qn = 0;
+                    pending = true;
+                }
+            } else {
+                drain(0);
+            }
+        };
+        auto resolve_pending = [&]() {
+            if (kDeferRound && FBM && pending) {
+                resolve();
+                pending = false;
+            }
+        };
         // Queue this lane's alive positions (bit r*8+j of `am` = position r*256 + lane*8 + j), one per
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
         // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
-        auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3) {
+        auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3, bool defer = false) {
             // The lanes' slots are the exclusive prefix of their counts c: from two ballots of the bits
             // of c when every c <= 3 (sparse groups: no shuffle chain), else a shuffle scan.  Each lane
             // then writes its own positions -- no ballot round per queued position.
@@ -702,7 +734,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                         (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
                 }
                 qn += total;
-                drain(0);
+                finish(defer);
                 return;
             }
             // dense groups (repetitive text): one queued position per lane and ballot round
@@ -718,7 +750,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 }
                 qn += __popc(b);
             }
-            drain(0);
+            finish(defer);
         };
         if (FBM && kP16 && lown == kSliceT && lend >= kSliceT + 16 + 16 && !(BAR && bar_slice)) {
             // interior slice, filter path, 16 positions per lane: one 64-bit window holds the 16
@@ -810,8 +842,10 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     }
                 }
             }
-            push(am, hg * 1024);
+            resolve_pending();  // the previous group's round: its J2 loads had this filter step to land
+            push(am, hg * 1024, 3, FBM);
           }
+          resolve_pending();
         } else if (BAR && bar_slice) {
             // Barrier path: a position whose K1-mer window touches a non-ACGT base cannot use the filter;
             // it is queued with the filter-flagged ones, and drain() bounds every walk at the next
