@@ -331,7 +331,8 @@ static __host__ __device__ constexpr uint32_t qcap_for(uint32_t bm_words) {
 #endif
 constexpr bool kPushScan = PFAC_PUSH_SCAN;
 #ifndef PFAC_DEFER
-#define PFAC_DEFER 1  // A/B knob: 0 = every group's queue drained before the next group's filter step
+#define PFAC_DEFER 0  // A/B knob: 1 = a group's last drain round resolved after the next group's filter
+                      // step (measured slower: cfg2 +2.4%, cfg3 +2%, cfg4 +6.7%, cfg5 +5%)
 #endif
 constexpr bool kDeferRound = PFAC_DEFER;
 #ifndef PFAC_MATCH_LOG
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 if (qn) {
                     __syncwarp();
                     issue(qn, 0);
+                    __syncwarp();  // the queue reads above before the next group's queue writes
                     qn = 0;
                     pending = true;
                 }

@@ -24,7 +24,7 @@ VARIANTS = {
     "ipl1": ["PFAC_DRAIN_IPL_1K=1"],
     "ipl3": ["PFAC_DRAIN_IPL_1K=3"],
     "ipl4": ["PFAC_DRAIN_IPL_1K=4"],         # A/B: one per lane in the 1024-position-slice kernels too
-    "nodefer": ["PFAC_DEFER=0"],             # A/B: every group's queue drained before the next group's filter step
+    "defer": ["PFAC_DEFER=1"],               # A/B: a group's last drain round resolved after the next group's filter step
     "chain16": ["PFAC_CHAIN32=0"],           # A/B: 16 forced bases per uint32 chain row (round 1)
     "noend": ["PFAC_ENDDEAD=0"],             # A/B: no end-state answers in uint32 chain rows
     "fb_add": ["PFAC_FB_LOP=0"],             # A/B: filter word addresses as base + offset (one more IADD per lookup)
