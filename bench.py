@@ -327,7 +327,8 @@ def run_pfac(args):
     text_plan = None
     if args.text_kernel is not None:
         a.set_text_kernel(args.text_kernel)
-    else:  # the library's text plan from a host sample of this rank's text (outside the timed region)
+    elif hasattr(P.lib(), "pfac_plan_text"):  # (A/B runs may load an older library without it)
+        # the library's text plan from a host sample of this rank's text (outside the timed region)
         stride = max(1, len(text) // 200_000)
         mode, deep = a.plan_text(text, stride=stride)
         text_plan = {"api": "pfac_plan_text", "sample_positions": -(-len(text) // stride),

@@ -19,7 +19,7 @@ done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference_${tag}.json 2>/dev/null
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${tag}.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-for c in 2 3 4 5; do
+for c in ${NCU_CFGS-2 3}; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 4 -c 1 \
     -o gpurun_out/match_text_cfg${c}_${tag} -f python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 done
@@ -31,5 +31,5 @@ for v in base merged_f tab_cg; do
       python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/abl_ncu_${v}_cfg${c}_${tag}.csv 2>/dev/null
   done
 done
-bash scripts/ab_libs.sh ${tag} 1 "2 3 4 5" base merged_f tab_cg r01
+bash scripts/ab_libs.sh ${tag} 2 "2 3 4 5" base merged_f tab_cg r01
 ls gpurun_out | grep ${tag} | wc -l
