@@ -316,7 +316,15 @@ void derive_host_image(pfac_automaton *a) {
             const Chain ch = chain_of(u, cell == 2 ? (uint32_t)kChainMax : (uint32_t)kChainMax32);
             const uint32_t nofin = ch.inner_final ? 0u : (cell == 2 ? 0x4000u : 0x40000000u);
             if (cell == 2) {
-                putc(im.T, (size_t)d * kRowCells + 0, chain_flag | nofin | ch.L);
+                // FSTEP: every state inside the span answers F(u) + its offset (nested prefix families
+                // with consecutive ids), so a walk that ends inside needs no F lookup
+                bool fstep = kFStep && ch.inner_final;  // (NOFIN rows answer F(u) anyway)
+                for (uint32_t j = 1, v = u, w2; fstep && j < ch.L; ++j) {
+                    unary_next(v, w2);
+                    v = w2;
+                    fstep = a->F[v] == a->F[u] + j;
+                }
+                putc(im.T, (size_t)d * kRowCells + 0, chain_flag | nofin | (fstep ? kFStep16 : 0u) | ch.L);
                 putc(im.T, (size_t)d * kRowCells + 1, (uint32_t)ch.bits & 0xFFFFu);
                 putc(im.T, (size_t)d * kRowCells + 2, (uint32_t)ch.bits >> 16);
                 putc(im.T, (size_t)d * kRowCells + 3, a->F[u]);

@@ -100,6 +100,7 @@ struct Row<uint16_t> {
     uint32_t f;  // PFAC_MERGED_F: F(s) from the row's cell 4
     __device__ __forceinline__ bool chain() const { return r.x & 0x8000u; }
     __device__ __forceinline__ bool nofin() const { return r.x & 0x4000u; }
+    __device__ __forceinline__ bool fstep() const { return r.x & kFStep16; }
     __device__ __forceinline__ uint32_t len() const { return r.x & 31u; }
     __device__ __forceinline__ uint32_t bits() const { return (r.x >> 16) | (r.y << 16); }
     __device__ __forceinline__ uint32_t fin() const { return r.y >> 16; }
@@ -248,6 +249,9 @@ __device__ __forceinline__ uint32_t walk(const Tab<CT, WIN> &tb, const uint32_t 
             if (m < lim || lim < L) {  // the walk ends inside this span, at s + min(m, lim)
                 const uint32_t mm = m < lim ? m : lim;
                 if (r.nofin() || mm == 0) return r.fin();
+                if constexpr (sizeof(CT) == 2) {
+                    if (r.fstep()) return r.fin() + mm;  // F(s + mm) = F(s) + mm along this span
+                }
                 s += mm;
                 break;
             }

@@ -45,6 +45,13 @@ constexpr int kChainMax32 = PFAC_CHAIN32 ? 32 : 16;
 #endif
 constexpr bool kEndDead = PFAC_ENDDEAD;
 constexpr uint32_t kChainLenMask32 = 63u, kEndShift = 6, kEndMask = 0xFFFFFFu;
+// uint16 chain rows: FSTEP (cell 0 bit 13) -- F(u + j) = F(u) + j for every j < L (nested prefix
+// families with consecutive ids), so a walk ending inside the span answers without an F lookup
+#ifndef PFAC_FSTEP
+#define PFAC_FSTEP 1  // A/B knob
+#endif
+constexpr bool kFStep = PFAC_FSTEP;
+constexpr uint32_t kFStep16 = 0x2000u;
 // Ablation (the paper's "two arrays vs one merged array"): PFAC_MERGED_F=1
 // stores F(s) in cell 4 of an 8-cell row next to the 4 transitions, so a walk that ends at a branch
 // state reads its answer from the row it already holds (rows twice as wide).  Default: T rows of 4

@@ -24,6 +24,7 @@ VARIANTS = {
     "ipl1": ["PFAC_DRAIN_IPL_1K=1"],
     "ipl3": ["PFAC_DRAIN_IPL_1K=3"],
     "ipl4": ["PFAC_DRAIN_IPL_1K=4"],         # A/B: one per lane in the 1024-position-slice kernels too
+    "nofstep": ["PFAC_FSTEP=0"],             # A/B: no FSTEP flag in uint16 chain rows
     "k2max10": ["PFAC_K2MAX=10"],            # A/B: second-level jump over 10-mers at most (4 MiB J2; cfg4 takes 11)
     "defer": ["PFAC_DEFER=1"],               # A/B: a group's last drain round resolved after the next group's filter step
     "chain16": ["PFAC_CHAIN32=0"],           # A/B: 16 forced bases per uint32 chain row (round 1)
