@@ -327,8 +327,6 @@ def run_pfac(args):
     text_plan = None
     if args.text_kernel is not None:
         a.set_text_kernel(args.text_kernel)
-    if args.emit_mode is not None:
-        a.set_emit_mode(args.emit_mode)
     elif hasattr(P.lib(), "pfac_plan_text"):  # (A/B runs may load an older library without it)
         # the library's text plan from a host sample of this rank's text (outside the timed region)
         stride = max(1, len(text) // 200_000)
@@ -668,8 +666,6 @@ def main():
                     help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")
     ap.add_argument("--all-matches", action="store_true",
                     help="add the all-occurrence expansion (pfac_expand_async) to the timed step")
-    ap.add_argument("--emit-mode", type=int, default=None, choices=[-1, 0, 1],
-                    help="pfac_set_emit_mode for the one-kernel text path (default: the library's plan)")
     ap.add_argument("--text-kernel", type=int, default=None, choices=[-1, 0, 1, 2],
                     help="pfac_set_text_kernel mode for the text path (default: the library's plan)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -224,15 +224,6 @@ uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int l
  * are identical in every mode; only the kernels differ.  PFAC_E_ARG for other modes or a null a.
  * The one mutable property of an automaton (an atomic; safe to change between calls). */
 int pfac_set_text_kernel(pfac_automaton *a, int mode);
-/* How the one-kernel text path builds the ordered match list (automaton `a`, all devices): mode
- * -1 = the plan's choice (default; pfac_plan_text), 0 = "runs": each warp matches a contiguous run
- * of slices, keeps its matches in a small staging area, then a per-warp match log, then re-reads its
- * out[] cells, and places them after one grid-wide prefix at the end; 1 = "rounds": warps take
- * slices in rounds of one slice each, publish each slice's match count, and write the previous
- * round's matches straight to their place in the list while they match the next round (no staging,
- * log or re-read; suits dense matches).  Results are identical in every mode.  PFAC_E_ARG for other
- * modes or a null a.  An atomic; safe to change between calls. */
-int pfac_set_emit_mode(pfac_automaton *a, int mode);
 /* A cheap statistic of a text for that policy (host memory, host code, no device work): the PFAC
  * walk (goto function only; a byte outside ACGTacgt has no transition, reading R5)
  * from positions 0, stride, 2*stride, ... < n of h_text, counting transitions.  *deep_frac = share

@@ -41,7 +41,6 @@ _SIGS = {
     "pfac_match_packed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_void_p, ctypes.c_void_p]),
     "pfac_set_text_kernel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
-    "pfac_set_emit_mode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "pfac_plan_text": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]),
     "pfac_text_walk_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
@@ -168,17 +167,14 @@ def _host_bytes(text) -> np.ndarray:
 # pfac_set_text_kernel mode applied to every new Automaton when its text_kernel argument is None
 # (None: the library's default, the plan's choice).  Tests switch it to cover every text path.
 DEFAULT_TEXT_KERNEL = None
-# pfac_set_emit_mode mode applied to every new Automaton when its emit_mode argument is None.
-DEFAULT_EMIT_MODE = None
 
 
 class Automaton:
     """pfac_build(patterns): the BFS-ordered automaton, finals numbered as pattern ids.
     text_kernel: pfac_set_text_kernel mode (-1 plan, 0 two kernels, 1 one kernel, 2 one kernel with
-    1024-position slices); None = DEFAULT_TEXT_KERNEL.  emit_mode: pfac_set_emit_mode mode (-1 plan,
-    0 runs, 1 rounds); None = DEFAULT_EMIT_MODE."""
+    1024-position slices); None = DEFAULT_TEXT_KERNEL."""
 
-    def __init__(self, patterns, text_kernel=None, emit_mode=None):
+    def __init__(self, patterns, text_kernel=None):
         data, offs = _flatten(patterns)
         h = ctypes.c_void_p()
         _check(lib().pfac_build(data.ctypes.data, offs.ctypes.data, len(offs) - 1, ctypes.byref(h)))
@@ -186,17 +182,10 @@ class Automaton:
         mode = DEFAULT_TEXT_KERNEL if text_kernel is None else text_kernel
         if mode is not None:
             self.set_text_kernel(mode)
-        emode = DEFAULT_EMIT_MODE if emit_mode is None else emit_mode
-        if emode is not None:
-            self.set_emit_mode(emode)
 
     def set_text_kernel(self, mode: int) -> None:
         """pfac_set_text_kernel: the path policy of match_text_async for this automaton."""
         _check(lib().pfac_set_text_kernel(self._h, int(mode)))
-
-    def set_emit_mode(self, mode: int) -> None:
-        """pfac_set_emit_mode: how the one-kernel text path builds the match list (-1 plan, 0 runs, 1 rounds)."""
-        _check(lib().pfac_set_emit_mode(self._h, int(mode)))
 
     def text_walk_stats(self, text, stride: int = 1, deep: int = 16) -> tuple[float, float]:
         """pfac_text_walk_stats on a host text (numpy uint8 / bytes / CPU tensor): (deep_frac,

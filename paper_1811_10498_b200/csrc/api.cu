@@ -336,13 +336,6 @@ int pfac_set_text_kernel(pfac_automaton *a, int mode) {
     return PFAC_OK;
 }
 
-int pfac_set_emit_mode(pfac_automaton *a, int mode) {
-    if (!a) return fail(PFAC_E_ARG, "pfac_set_emit_mode: null automaton");
-    if (mode < -1 || mode > 1) return fail(PFAC_E_ARG, "pfac_set_emit_mode: mode must be -1, 0 or 1");
-    a->emit_mode.store(mode, std::memory_order_relaxed);
-    return PFAC_OK;
-}
-
 int pfac_text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_t n, uint64_t stride, uint32_t deep,
                          double *deep_frac, double *mean_steps) {
     return text_walk_stats(a, h_text, n, stride, deep, deep_frac, mean_steps);
@@ -492,10 +485,9 @@ static int match_text_impl(const pfac_automaton *a, DeviceImage &imr, const uint
     int e;
     const int tk = text_kernel_for(a, *im);
     if (tk && aligned16(d_text)) {
-        const bool rnd = a->emit_mode.load(std::memory_order_relaxed) == 1;
         e = launch_match_compact(*im, a->k, nullptr, nullptr, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
                                  d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad, nullptr,
-                                 tk == 2, rnd);
+                                 tk == 2);
     } else {  // two kernels through the workspace (unaligned text, or a halo too long for the plan)
         // pack records the first bad index over the readable text; the fused kernel skips the barrier
         // bits when there is none and writes the owned part of it to d_first_bad

@@ -30,7 +30,6 @@ struct CompactArgs {
     uint8_t *log;         // fused kernel: per-warp match logs (log_pw bytes each, 16-byte multiple)
     uint64_t log_pw;
     uint32_t pid16;       // log pids as uint16 (every id < 2^16)
-    uint64_t *agg;        // RND: per (round, CTA) arrivals << 40 | match count (zeroed per call)
 };
 
 // NC: out[] was written by an earlier launch (read-only here: ld.global.nc); otherwise (the fused

@@ -343,9 +343,6 @@ constexpr bool kDeferRound = PFAC_DEFER;
 #define PFAC_MATCH_LOG 1  // A/B knob: 0 = no per-warp match log (a full staging area spills at once)
 #endif
 constexpr bool kMatchLog = PFAC_MATCH_LOG;
-#ifndef PFAC_RND_NOWAIT
-#define PFAC_RND_NOWAIT 0  // probe only (wrong lists): the round emission without its waits
-#endif
 constexpr int kFBK = kFilterK;                         // filter length K1 (FBM)
 constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared memory (4^10: 128 KiB)
 
@@ -363,7 +360,7 @@ static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, b
 }
 
 template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false, bool TXT = false,
-          uint32_t SL = kSlice, bool RND = false>
+          uint32_t SL = kSlice>
 __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // positions per slice (text kernel for large automata: 1024, which leaves L1 more room)
     static_assert(SL % 1024 == 0 && SL <= 65536, "slice = whole 1024-position groups, u16 positions");
@@ -372,7 +369,6 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
-    static_assert(!RND || TXT, "in-order emission by rounds: the text kernel");
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
@@ -417,8 +413,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     const uint64_t gw = (uint64_t)blockIdx.x * kMWarps + warp;
     // slice schedule: strided over the grid, or (fused) a contiguous run per warp so that the warp's
     // matches come out in position order
-    // RND (emission by rounds): strided, so that a round of TW consecutive slices is done together
-    constexpr bool CONTIG = !RND && (FUSE || kContiguousSchedule);
+    constexpr bool CONTIG = FUSE || kContiguousSchedule;
     // contiguous runs balanced to within one slice: warp gw owns [gw*N/TW, (gw+1)*N/TW) (a ceil-sized
     // run per warp would leave the last warps idle: cfg2 has 30.2 slices per warp)
 #if PFAC_BALANCED
@@ -495,115 +490,6 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     bool bad_done = false;    // TXT: this warp has reported its first non-ACGT byte (slices ascend)
     uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
     uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
-    // RND: in-order emission by rounds.  Round r = slices [r TW, (r+1) TW), slice r TW + gw on warp gw.
-    // When a warp has matched a slice it publishes the slice's match count -- in shared memory for the
-    // warps of its CTA (a 4-round ring, tag = round + 1) and added to the CTA's count of that round in
-    // global memory (p.c.agg, arrivals << 40 | count; relaxed: the values are the only message) -- and then emits the slice it matched
-    // one round earlier: once every CTA's count of that round is complete, its list offset is the total
-    // of the rounds before it + the counts of the CTAs and warps before it, and its matches go straight
-    // to the list (positions from its bitmap, kept in registers; ids re-read from its out[] cells, which
-    // this warp wrote one slice ago: L2 hits).  No staging, no log, no re-read after a grid-wide prefix.
-    constexpr uint32_t kRW = RND ? kBmWordsT / 32 : 1;  // bitmap words per lane of a slice
-    uint32_t *rnd_ring = reinterpret_cast<uint32_t *>(s_wcount);  // [4][kMWarps] (the grid_prefix area)
-    uint64_t rnd_base = 0;    // matches of the rounds before the next one this warp emits
-    uint64_t d_sl = ~0ull;    // the slice matched but not yet emitted (~0: none)
-    uint32_t d_cnt = 0, d_bm[kRW];
-#pragma unroll
-    for (uint32_t h = 0; h < kRW; ++h) d_bm[h] = 0;
-    (void)rnd_ring;
-    auto rnd_emit = [&]() {
-        const uint64_t rd = d_sl / TW;
-        // every CTA's count of round rd (spin until its warps with a slice in rd have arrived)
-        const uint64_t *ag = p.c.agg + rd * gridDim.x;
-        uint64_t pre = 0, tot = 0;
-        for (uint32_t c0 = 0; c0 < gridDim.x; c0 += 32) {
-            const uint32_t c = c0 + lane;
-            uint64_t x = 0;
-            if (c < gridDim.x) {
-                const uint64_t first = rd * TW + (uint64_t)c * kMWarps;
-                const uint64_t expect = first >= p.nslices ? 0 : (p.nslices - first < kMWarps ? p.nslices - first : kMWarps);
-                if (expect) {
-                    uint64_t v = ld_relaxed_u64(ag + c);
-                    while (!PFAC_RND_NOWAIT && (v >> 40) < expect) {
-                        __nanosleep(64);
-                        v = ld_relaxed_u64(ag + c);
-                    }
-                    x = v & ((1ull << 40) - 1);
-                }
-            }
-            tot += x;
-            pre += c < blockIdx.x ? x : 0ull;
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            pre += __shfl_xor_sync(~0u, pre, d);
-            tot += __shfl_xor_sync(~0u, tot, d);
-        }
-        // the warps before this one in its CTA (spin on the ring entry's round tag)
-        uint32_t wv = 0;
-        if (lane < warp) {
-            const uint32_t tag = (uint32_t)(rd + 1) & 0xFFFFFu;
-            const volatile uint32_t *e = rnd_ring + (rd & 3) * kMWarps + lane;
-            uint32_t v = *e;
-            while (!PFAC_RND_NOWAIT && (v >> 12) != tag) v = *e;
-            wv = v & 0xFFFu;
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) wv += __shfl_xor_sync(~0u, wv, d);
-        const uint64_t off = rnd_base + pre + wv;
-        rnd_base += tot;
-        if (d_sl == p.nslices - 1 && lane == 0) *p.c.d_count = off + d_cnt;
-        if (!d_cnt) return;
-        const uint64_t dbase = d_sl * kSliceT;
-        const uint64_t own_left = p.n_own - dbase;
-        const uint32_t dlown = own_left < kSliceT ? (uint32_t)own_left : kSliceT;
-        const int32_t *dout = p.out + dbase;
-        const uint64_t pbase = p.c.pos_base + dbase;
-        // 128-position steps with a match: step h*8 + j covers words 32h + 4j .. +3 (word 32h + t: lane t's d_bm[h])
-        uint32_t smask = 0;
-#pragma unroll
-        for (uint32_t h = 0; h < kRW; ++h) {
-            const uint32_t b = __ballot_sync(~0u, d_bm[h] != 0);
-#pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) smask |= ((b >> (4 * j)) & 0xFu) ? 1u << (h * 8 + j) : 0u;
-        }
-        auto ld4 = [&](uint32_t ch) -> uint4 {  // this warp's stores of one slice ago: coherent L2 loads
-            const uint32_t l0 = ch * 128 + lane * 4;
-            return l0 + 4 <= dlown ? ld_cg_v4(dout + l0) : make_uint4(0, 0, 0, 0);
-        };
-        uint64_t r0 = off;
-        uint32_t ch = __ffs(smask) - 1;
-        smask &= smask - 1;
-        uint4 q = ld4(ch);
-#pragma unroll 1
-        while (true) {
-            const bool more = smask != 0;
-            const uint32_t chn = more ? __ffs(smask) - 1 : 0u;
-            smask &= smask - 1;
-            const uint4 qn = more ? ld4(chn) : make_uint4(0, 0, 0, 0);  // the next step's loads first
-            uint32_t wsrc = d_bm[0];
-#pragma unroll
-            for (uint32_t h = 1; h < kRW; ++h) wsrc = (ch >> 3) == h ? d_bm[h] : wsrc;
-            const uint32_t m = (__shfl_sync(~0u, wsrc, (ch & 7) * 4 + (lane >> 3)) >> ((lane & 7) * 4)) & 0xFu;
-            uint32_t tot4;
-            uint64_t r = r0 + nibble_rank(m, lt, tot4);
-            if (m) {
-                const uint32_t l0 = ch * 128 + lane * 4;
-                uint32_t v[4] = {q.x, q.y, q.z, q.w};
-                if (l0 + 4 > dlown) {  // the slice's last owned cells
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) v[e] = (m >> e) & 1 ? ld_cg_u32(dout + l0 + e) : 0u;
-                }
-#pragma unroll
-                for (uint32_t e = 0; e < 4; ++e)
-                    if ((m >> e) & 1) put_match(p.c, r++, pbase + l0 + e, v[e]);
-            }
-            r0 += tot4;
-            if (!more) break;
-            ch = chn;
-            q = qn;
-        }
-    };
     for (uint64_t sl = s_first; sl < s_end; sl += s_stride, ++it) {
         const uint32_t buf = it & 1;
         if (!TXT && lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
@@ -1069,26 +955,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         }
         __syncwarp();  // all lanes done with `txt` before lane 0 refills it next iteration
         if constexpr (TXT) pred_bar = bar_slice;
-        if constexpr (RND) {  // publish this slice's count, emit the previous one (see rnd_emit)
-            uint32_t nb[kRW], cnt = 0;
-#pragma unroll
-            for (uint32_t h = 0; h < kRW; ++h) {
-                nb[h] = bm[h * 32 + lane];
-                cnt += __popc(nb[h]);
-            }
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
-            if (lane == 0) {
-                const uint64_t r = sl / TW;
-                *reinterpret_cast<volatile uint32_t *>(rnd_ring + (r & 3) * kMWarps + warp) = ((uint32_t)(r + 1) << 12) | cnt;
-                red_relaxed_add_u64(p.c.agg + r * gridDim.x + blockIdx.x, (1ull << 40) | cnt);
-            }
-            if (d_sl != ~0ull) rnd_emit();
-            d_sl = sl;
-            d_cnt = cnt;
-#pragma unroll
-            for (uint32_t h = 0; h < kRW; ++h) d_bm[h] = nb[h];
-        } else if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
+        if (FUSE) {  // stage this slice's matches in position order (word w = positions 32w..32w+31)
             uint32_t any = 0;
             for (uint32_t w = lane; w < kBmWordsT; w += 32) any |= bm[w];
             uint32_t cnt = 0;
@@ -1187,9 +1054,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // TXT: a warp that had no slice never waited for the table copy; no CTA may retire while its
     // bulk copy into shared memory is in flight
     if (TXT && it == 0) mbar_wait(tab_bar, 0);
-    if constexpr (RND) {
-        if (d_sl != ~0ull) rnd_emit();
-    } else if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
+    if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
         const uint64_t prefix = grid_prefix<kMWarps>(wcount, p.c.counts, p.c.d_count, s_wcount, s_woff);
         for (uint64_t i = lane; i < wstaged; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);
         // logged slices, in slice order: positions from each record's bitmap, pids from its list
@@ -1387,31 +1252,26 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
 }
 
 template <typename CT, bool LIST, uint32_t SL = kSlice>
-static const void *txt_kernel(bool all_smem, bool rnd) {
-    constexpr int K = sizeof(CT) == 2 ? kJumpK16 : kJumpK32;
-    if (rnd)
-        return all_smem ? (const void *)match_kernel<CT, false, K, true, true, true, LIST, true, SL, true>
-                        : (const void *)match_kernel<CT, true, K, true, true, true, LIST, true, SL, true>;
-    return all_smem ? (const void *)match_kernel<CT, false, K, true, true, true, LIST, true, SL>
-                    : (const void *)match_kernel<CT, true, K, true, true, true, LIST, true, SL>;
+static const void *txt_kernel(bool all_smem) {
+    return all_smem ? (const void *)match_kernel<CT, false, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL>
+                    : (const void *)match_kernel<CT, true, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL>;
 }
 
 template <bool FUSE>
 static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false, bool txt = false,
-                              bool small = false, bool rnd = false) {
+                              bool small = false) {
     const MatchPlan &pl = img.plan;
     if constexpr (FUSE) {
         if (txt && small) {  // text input, 1024-position slices
             if (pl.cell == 2)
-                return list ? txt_kernel<uint16_t, true, kSliceSmall>(pl.all_smem_txt1k, rnd)
-                            : txt_kernel<uint16_t, false, kSliceSmall>(pl.all_smem_txt1k, rnd);
-            return list ? txt_kernel<uint32_t, true, kSliceSmall>(pl.all_smem_txt1k, rnd)
-                        : txt_kernel<uint32_t, false, kSliceSmall>(pl.all_smem_txt1k, rnd);
+                return list ? txt_kernel<uint16_t, true, kSliceSmall>(pl.all_smem_txt1k)
+                            : txt_kernel<uint16_t, false, kSliceSmall>(pl.all_smem_txt1k);
+            return list ? txt_kernel<uint32_t, true, kSliceSmall>(pl.all_smem_txt1k)
+                        : txt_kernel<uint32_t, false, kSliceSmall>(pl.all_smem_txt1k);
         }
         if (txt) {  // text input (filter path; checked by the launcher)
-            if (pl.cell == 2)
-                return list ? txt_kernel<uint16_t, true>(pl.all_smem_txt, rnd) : txt_kernel<uint16_t, false>(pl.all_smem_txt, rnd);
-            return list ? txt_kernel<uint32_t, true>(pl.all_smem_txt, rnd) : txt_kernel<uint32_t, false>(pl.all_smem_txt, rnd);
+            if (pl.cell == 2) return list ? txt_kernel<uint16_t, true>(pl.all_smem_txt) : txt_kernel<uint16_t, false>(pl.all_smem_txt);
+            return list ? txt_kernel<uint32_t, true>(pl.all_smem_txt) : txt_kernel<uint32_t, false>(pl.all_smem_txt);
         }
         if (list) {  // list-only (filter path only; checked by the launcher)
             if (bar) {
@@ -1499,9 +1359,8 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only, const uint8_t *d_text, uint64_t *d_first_bad,
-                         const uint64_t *d_bad_all, bool small, bool rnd) {
+                         const uint64_t *d_bad_all, bool small) {
     small = small && d_text;  // 1024-position slices: the text kernel only
-    rnd = rnd && d_text;      // emission by rounds: the text kernel only
     cudaStream_t st = (cudaStream_t)stream;
     if (d_first_bad && (d_text || n_own == 0)) {
         cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, 8, st);
@@ -1542,14 +1401,10 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.log_pw = kMatchLog ? (match_log_bytes(n_own) / warps) & ~15ull : 0;
     c.pid16 = k < 65536u;
     c.chunk = a.slices_per_warp * slice;
-    // RND: the (round, CTA) counts live in the staging area (rounds * grid * 8 <= its 12 B per entry)
-    c.agg = c.stage_pos;
-    const uint64_t rounds = (a.nslices + warps - 1) / warps;
-    cudaError_t e = rnd ? cudaMemsetAsync(c.agg, 0, (size_t)(rounds * grid * 8), st)
-                        : cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
+    cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr, small, rnd), grid, a,
-                  true, st, small);
+    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr, small), grid, a, true,
+                  st, small);
 }
 
 }  // namespace pfac

@@ -171,7 +171,6 @@ struct pfac_automaton {
     std::vector<uint32_t> prefix_flat; // every pattern's chain, shortest first, at its flat base
     pfac::HostImage host_image;   // derived once at build
     std::atomic<int> text_kernel{-1};  // pfac_set_text_kernel: -1 = the plan's choice, else forced 0/1/2
-    std::atomic<int> emit_mode{-1};    // pfac_set_emit_mode: -1 = the plan's choice, 0 = runs, 1 = rounds
     std::mutex mu;                // guards images
     std::vector<pfac::DeviceImage *> images;
 };
@@ -200,7 +199,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only = false, const uint8_t *d_text = nullptr,
                          uint64_t *d_first_bad = nullptr, const uint64_t *d_bad_all = nullptr,
-                         bool small = false, bool rnd = false);
+                         bool small = false);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
                   const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,

@@ -29,7 +29,6 @@ VARIANTS = {
     "defer": ["PFAC_DEFER=1"],               # A/B: a group's last drain round resolved after the next group's filter step
     "chain16": ["PFAC_CHAIN32=0"],           # A/B: 16 forced bases per uint32 chain row (round 1)
     "noend": ["PFAC_ENDDEAD=0"],             # A/B: no end-state answers in uint32 chain rows
-    "rnd_nowait": ["PFAC_RND_NOWAIT=1"],     # probe: the round emission (emit mode 1) without its waits (wrong lists)
     "fb_add": ["PFAC_FB_LOP=0"],             # A/B: filter word addresses as base + offset (one more IADD per lookup)
 }
 

@@ -242,10 +242,6 @@ def _oracle_chunk(ab):
     return Oracle(pats).match_list(text, ab[0], ab[1])
 
 
-# (pfac_set_text_kernel, pfac_set_emit_mode) pairs: every path of the text call
-TEXT_PATHS = ((1, 0), (0, 0), (2, 0), (1, 1), (2, 1))
-
-
 def _full_config(idx):
     cfg = gen.CONFIGS[idx]
     pats = gen.config_patterns(cfg)
@@ -285,9 +281,8 @@ def _full_config(idx):
     del packed, ws
     # the text-input call (pack fused into the kernel; the bench default where the plan takes it) in
     # both of its paths, on the same full input: list, count, first_bad and the whole dense out[]
-    for mode, emit in TEXT_PATHS:
+    for mode in (1, 0, 2):
         a.set_text_kernel(mode)
-        a.set_emit_mode(emit)
         ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
         out3 = torch.empty(n, dtype=torch.int32, device=DEV)
         bad = torch.zeros(1, dtype=torch.int64, device=DEV)
@@ -300,7 +295,6 @@ def _full_config(idx):
         assert bool((out3 == out).all())
         del out3, ws
     a.set_text_kernel(-1)
-    a.set_emit_mode(-1)
     # sampled out[] windows (every element, including the zeros)
     o = Oracle(pats)
     n = len(text)
@@ -457,9 +451,8 @@ def test_config2_fasta_full_text_kernel():
     epos, epid = _oracle_list_parallel(pats, text)
     bad_idx = int(np.nonzero(~np.isin(text[:1000], np.frombuffer(b"ACGTacgt", np.uint8)))[0][0])
     o = Oracle(pats)
-    for mode, emit in ((1, 0), (0, 0), (1, 1)):
+    for mode in (1, 0):
         a.set_text_kernel(mode)
-        a.set_emit_mode(emit)
         out = torch.empty(n, dtype=torch.int32, device=DEV)
         cap = len(epos) + 1024
         pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)
@@ -491,9 +484,8 @@ def test_text_beyond_2pow32_positions():
     epos, epid = _oracle_list_parallel(pats, text)
     assert len(epos) > 1_000_000 and int(epos[-1]) > (1 << 32)
     o = Oracle(pats)
-    for mode, emit in ((1, 0), (0, 0), (1, 1)):
+    for mode in (1, 0):
         a.set_text_kernel(mode)
-        a.set_emit_mode(emit)
         out = torch.empty(n, dtype=torch.int32, device=DEV)
         cap = len(epos) + 1024
         pos = torch.full((cap,), -1, dtype=torch.int64, device=DEV)

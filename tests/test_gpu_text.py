@@ -27,16 +27,13 @@ ACGT8 = np.frombuffer(b"ACGTacgt", np.uint8)
 U64MAX = (1 << 64) - 1
 
 
-@pytest.fixture(autouse=True, params=["1", "0", "2", "1r", "2r"],
-                ids=["one-kernel", "two-kernel", "one-kernel-1k", "one-kernel-rounds", "one-kernel-1k-rounds"])
+@pytest.fixture(autouse=True, params=["1", "0", "2"], ids=["one-kernel", "two-kernel", "one-kernel-1k"])
 def text_kernel(request, monkeypatch):
     """Both paths of pfac_match_text_async: the one-kernel TXT instantiation and the pack + fused
     kernel path the call takes for unaligned text or automata the policy keeps off TXT; "2": the text
-    kernel with 1024-position slices (both cell widths); "r": the text kernel emitting its list by
-    rounds (pfac_set_emit_mode 1) instead of per-warp runs."""
-    monkeypatch.setattr(P.binding, "DEFAULT_TEXT_KERNEL", int(request.param[0]))
-    monkeypatch.setattr(P.binding, "DEFAULT_EMIT_MODE", 1 if request.param.endswith("r") else 0)
-    return request.param[0]
+    kernel with 1024-position slices (both cell widths)."""
+    monkeypatch.setattr(P.binding, "DEFAULT_TEXT_KERNEL", int(request.param))
+    return request.param
 
 
 def first_bad(text: np.ndarray, n_own: int) -> int:
