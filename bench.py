@@ -379,7 +379,7 @@ def run_pfac(args):
     # text path: one kernel when the image's plan takes it (pfac_image_info.text_kernel), else pack +
     # first-bad scan + fused kernel inside the call
     text_variant = a.image_info(local)["text_kernel"] if text_in and d_text.data_ptr() % 16 == 0 else 0
-    text_one = text_variant in (1, 2)
+    text_one = text_variant in (1, 2, 3)
     kernels_per_step = (1 if text_one else 3 if text_in else 2 if fused else 3) + (1 if args.all_matches else 0)
     if args.all_matches:  # every occurrence: size the output from a probe
         ws_e = torch.empty(P.expand_workspace_bytes(), dtype=torch.uint8, device=dev)
@@ -610,7 +610,7 @@ def run_pfac(args):
                        **({"text_plan": text_plan} if text_plan else {})},
             "roofline": {"bound": "hbm", "achieved": match_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": match_gbs / hbm, "traffic": traffic,
-                         "kernel": ("match_kernel<TXT=1" + (", 1024-position slices" if text_variant == 2 else "") +
+                         "kernel": ("match_kernel<TXT=1" + ({2: ", 1024-position slices", 3: ", 1024-position slices claimed dynamically"}.get(text_variant, "")) +
                                     "> (pack + match + compact)" if text_one and not list_only else
                                     "match_kernel<TXT=1, list-only> (pack + match + list)" if text_one else
                                     "pack + match_kernel<FUSE=1,BAR=1> (two-kernel text path)" if text_in else
@@ -666,7 +666,7 @@ def main():
                     help="FASTA-like text: a newline every LINE bases + N gaps; runs the barrier kernels")
     ap.add_argument("--all-matches", action="store_true",
                     help="add the all-occurrence expansion (pfac_expand_async) to the timed step")
-    ap.add_argument("--text-kernel", type=int, default=None, choices=[-1, 0, 1, 2],
+    ap.add_argument("--text-kernel", type=int, default=None, choices=[-1, 0, 1, 2, 3],
                     help="pfac_set_text_kernel mode for the text path (default: the library's plan)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -220,8 +220,11 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
 uint64_t pfac_match_text_workspace_bytes(uint64_t n_own, uint64_t n_avail, int list_only);
 /* Path policy of pfac_match_text_async for automaton `a` (all devices): mode -1 = the plan's
  * measured choice (default), 0 = always pack -> fused kernel, 1 = the one-kernel path whenever it
- * fits (2048-position slices first), 2 = its 1024-position-slice form whenever it fits.  Results
- * are identical in every mode; only the kernels differ.  PFAC_E_ARG for other modes or a null a.
+ * fits (2048-position slices first), 2 = its 1024-position-slice form whenever it fits, 3 = that
+ * form with the slices claimed dynamically by the warps (a global counter) instead of a fixed run
+ * per warp, the matches placed after a scan of per-slice counts at the end (load balance for text
+ * whose per-slice walk work varies widely).  Results are identical in every mode; only the kernels
+ * differ.  PFAC_E_ARG for other modes or a null a.
  * The one mutable property of an automaton (an atomic; safe to change between calls). */
 int pfac_set_text_kernel(pfac_automaton *a, int mode);
 /* A cheap statistic of a text for that policy (host memory, host code, no device work): the PFAC
@@ -235,9 +238,11 @@ int pfac_text_walk_stats(const pfac_automaton *a, const uint8_t *h_text, uint64_
 /* The text-call path from a text sample (host memory; host code, no device work): the walk statistic
  * above (deep = 16, every stride-th position) decides -- walk-heavy text (>= 1% of the sampled walks
  * make 16 or more transitions: repetitive text against nested patterns) takes the 1024-position-slice
- * text kernel (mode 2), whose smaller per-warp staging leaves shared memory for a row window and L1
- * room for rows (measured on cfg5: 3.61 ms vs 3.96 ms with 2048-position slices and 3.69 ms for pack +
- * fused); other text keeps the automaton's plan (mode -1).  Applies the mode with
+ * text kernel with dynamically claimed slices (mode 3): its smaller per-warp staging leaves shared
+ * memory for a row window and L1 room for rows, and claiming balances the widely varying per-slice
+ * walk work (measured on cfg5: 3.10 ms vs 3.54 ms with a fixed run per warp (mode 2), 3.96 ms with
+ * 2048-position slices); other text keeps the automaton's plan (mode -1: on such text mode 3's
+ * interleaved out[] write streams cost cfg2 +40%, cfg4 +26%).  Applies the mode with
  * pfac_set_text_kernel and returns it in *mode (nullable), the statistic in *deep_frac (nullable).
  * Errors as pfac_text_walk_stats. */
 int pfac_plan_text(pfac_automaton *a, const uint8_t *h_sample, uint64_t n, uint64_t stride, int *mode,
@@ -304,7 +309,8 @@ typedef struct {
     uint64_t l2_persist_bytes;/* access-policy window over J2 + the chain-head rows HR */
     uint64_t image_bytes;     /* device memory of the image (all tables, HR and prefix chains) */
     uint32_t text_kernel;     /* pfac_match_text_async on aligned text: 0 = pack + fused kernel,
-                                 1 = one kernel, 2 = one kernel with 1024-position slices */
+                                 1 = one kernel, 2 = one kernel with 1024-position slices,
+                                 3 = that kernel with dynamically claimed slices */
     uint32_t text_window_rows;/* rows staged in shared memory by that kernel */
     uint32_t hr_rows;         /* chain-head row copies next to J2 (uint32 images; 0 = none) */
     uint32_t hr_nb_rows;      /* of which NOFIN chains whose J2 entry carries their first 4 bases

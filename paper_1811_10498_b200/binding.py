@@ -172,7 +172,7 @@ DEFAULT_TEXT_KERNEL = None
 class Automaton:
     """pfac_build(patterns): the BFS-ordered automaton, finals numbered as pattern ids.
     text_kernel: pfac_set_text_kernel mode (-1 plan, 0 two kernels, 1 one kernel, 2 one kernel with
-    1024-position slices); None = DEFAULT_TEXT_KERNEL."""
+    1024-position slices, 3 the same with dynamically claimed slices); None = DEFAULT_TEXT_KERNEL."""
 
     def __init__(self, patterns, text_kernel=None):
         data, offs = _flatten(patterns)

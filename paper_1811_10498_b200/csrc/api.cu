@@ -331,7 +331,7 @@ int pfac_match_packed(const pfac_automaton *a, const uint32_t *d_packed, uint64_
 
 int pfac_set_text_kernel(pfac_automaton *a, int mode) {
     if (!a) return fail(PFAC_E_ARG, "pfac_set_text_kernel: null automaton");
-    if (mode < -1 || mode > 2) return fail(PFAC_E_ARG, "pfac_set_text_kernel: mode must be -1, 0, 1 or 2");
+    if (mode < -1 || mode > 3) return fail(PFAC_E_ARG, "pfac_set_text_kernel: mode must be -1, 0, 1, 2 or 3");
     a->text_kernel.store(mode, std::memory_order_relaxed);
     return PFAC_OK;
 }
@@ -349,7 +349,7 @@ int pfac_plan_text(pfac_automaton *a, const uint8_t *h_sample, uint64_t n, uint6
     double df = 0, ms = 0;
     const int rc = text_walk_stats(a, h_sample, n, stride, kDeepWalk, &df, &ms);
     if (rc != PFAC_OK) return rc;
-    const int m = df >= kWalkHeavyShare ? 2 : -1;
+    const int m = df >= kWalkHeavyShare ? 3 : -1;
     a->text_kernel.store(m, std::memory_order_relaxed);
     if (mode) *mode = m;
     if (deep_frac) *deep_frac = df;
@@ -418,14 +418,14 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
 static uint64_t al16(uint64_t x) { return (x + 15) & ~15ull; }
 
 // Which path pfac_match_text_async runs for this image: 0 = pack -> fused kernel, 1 = the text kernel,
-// 2 = the text kernel with 1024-position slices.  The plan's measured preference (MatchPlan::txt_pref,
+// 2 = the text kernel with 1024-position slices, 3 = that kernel with slices claimed dynamically.  The plan's measured preference (MatchPlan::txt_pref,
 // txt1k_pref), unless pfac_set_text_kernel forced 0 (never) / 1 (whenever one fits; 2048 slices
 // first) / 2 (1024 slices whenever they fit).
 static int text_kernel_for(const pfac_automaton *a, const DeviceImage &im) {
     const int force = a->text_kernel.load(std::memory_order_relaxed);
     const MatchPlan &pl = im.plan;
     if (!im.K2 || force == 0) return 0;
-    if (force == 2) return pl.txt1k_ok ? 2 : 0;
+    if (force == 2 || force == 3) return pl.txt1k_ok ? force : 0;
     if (force == 1) return pl.txt_ok ? 1 : pl.txt1k_ok ? 2 : 0;
     return pl.txt_pref ? 1 : pl.txt1k_pref ? 2 : 0;
 }
@@ -487,7 +487,7 @@ static int match_text_impl(const pfac_automaton *a, DeviceImage &imr, const uint
     if (tk && aligned16(d_text)) {
         e = launch_match_compact(*im, a->k, nullptr, nullptr, n_own, n_avail, out, pos_base, d_pos, d_pid, capacity,
                                  d_count, d_hist, d_workspace, stream, list_only, d_text, d_first_bad, nullptr,
-                                 tk == 2);
+                                 tk >= 2, tk == 3);
     } else {  // two kernels through the workspace (unaligned text, or a halo too long for the plan)
         // pack records the first bad index over the readable text; the fused kernel skips the barrier
         // bits when there is none and writes the owned part of it to d_first_bad

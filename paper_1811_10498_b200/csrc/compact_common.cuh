@@ -30,6 +30,9 @@ struct CompactArgs {
     uint8_t *log;         // fused kernel: per-warp match logs (log_pw bytes each, 16-byte multiple)
     uint64_t log_pw;
     uint32_t pid16;       // log pids as uint16 (every id < 2^16)
+    uint32_t *scnt;       // DYN: per-slice match count (bit 31: spilled)
+    uint64_t *soff;       // DYN: per-slice list offset (the scan of scnt)
+    uint64_t *ctl;        // DYN: [0] slice claim counter, [1], [2] grid barriers (zeroed per call)
 };
 
 // NC: out[] was written by an earlier launch (read-only here: ld.global.nc); otherwise (the fused

@@ -55,9 +55,16 @@ namespace pfac {
 #ifndef PFAC_PH1_UNROLL
 #define PFAC_PH1_UNROLL 1
 #endif
+#ifndef PFAC_MT_1K
+#define PFAC_MT_1K PFAC_MT
+#endif
 constexpr int kMT = PFAC_MT;                // threads per CTA (A/B knob)
 constexpr int kPh1Unroll = PFAC_PH1_UNROLL; // sub-slices unrolled in the lookup phase (A/B knob)
 constexpr int kMWarps = kMT / 32;
+// threads per CTA of the 1024-position-slice text kernels (A/B knob: their smaller per-warp buffers leave
+// the shared memory for more warps)
+static __host__ __device__ constexpr int mt_for(uint32_t slice) { return slice == 1024 ? PFAC_MT_1K : kMT; }
+static_assert(PFAC_MT_1K % 32 == 0 && PFAC_MT_1K <= 1024, "whole warps, <= 32 per CTA (grid_prefix)");
 constexpr uint32_t kP = 8;                  // consecutive positions per lane per sub-slice
 constexpr uint32_t kSubN = 32 * kP;         // 256 positions per sub-slice
 #ifndef PFAC_SLICE
@@ -137,6 +144,46 @@ __device__ __forceinline__ T ld_tab(const T *p) {
 #endif
 }
 
+// L1::no_allocate forms (A/B knobs PFAC_J2_NA: J2 and HR loads; PFAC_TAB_NA: every table load): the
+// lookups of large automata are random over megabytes, so an L1 line allocated per miss buys no reuse
+#ifndef PFAC_J2_NA
+#define PFAC_J2_NA 0
+#endif
+#ifndef PFAC_TAB_NA
+#define PFAC_TAB_NA 0
+#endif
+__device__ __forceinline__ uint32_t ld_na(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_na(const uint2 *p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_na(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint16_t ld_na(const uint16_t *p) {
+    uint16_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T ld_row(const T *p) {  // T rows and F entries
+    if constexpr (PFAC_TAB_NA) return ld_na(p);
+    else return ld_tab(p);
+}
+template <typename T>
+__device__ __forceinline__ T ld_j2(const T *p) {  // J2 entries and chain-head row copies
+    if constexpr (PFAC_TAB_NA || PFAC_J2_NA) return ld_na(p);
+    else return ld_tab(p);
+}
+
 template <typename CT, bool WIN>
 struct Tab {
     const CT *Tw, *Fw, *Tg, *Fg;
@@ -145,17 +192,17 @@ struct Tab {
         Row<CT> r;
         if constexpr (sizeof(CT) == 2 && kMergedF) {  // one 16-byte row: 4 transitions, F, padding
             const uint4 v = (!WIN || s < W) ? *reinterpret_cast<const uint4 *>(Tw + (size_t)s * kRowCells)
-                                            : ld_tab(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
+                                            : ld_row(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
             r.r = make_uint2(v.x, v.y);
             r.f = v.z & 0xFFFFu;
         } else if constexpr (sizeof(CT) == 2) {
             if (!WIN || s < W) r.r = *reinterpret_cast<const uint2 *>(Tw + (size_t)s * kRowCells);
-            else r.r = ld_tab(reinterpret_cast<const uint2 *>(Tg + (size_t)s * kRowCells));
+            else r.r = ld_row(reinterpret_cast<const uint2 *>(Tg + (size_t)s * kRowCells));
         } else {
             if (!WIN || s < W) r.r = *reinterpret_cast<const uint4 *>(Tw + (size_t)s * kRowCells);
-            else r.r = ld_tab(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
+            else r.r = ld_row(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
             if constexpr (kMergedF)
-                r.f = (!WIN || s < W) ? (uint32_t)Tw[(size_t)s * kRowCells + 4] : (uint32_t)ld_tab(Tg + (size_t)s * kRowCells + 4);
+                r.f = (!WIN || s < W) ? (uint32_t)Tw[(size_t)s * kRowCells + 4] : (uint32_t)ld_row(Tg + (size_t)s * kRowCells + 4);
         }
         return r;
     }
@@ -163,11 +210,11 @@ struct Tab {
         if constexpr (kMergedF) {
             const size_t b = (size_t)s * kRowCells + 4;
             if constexpr (!WIN) return Tw[b];
-            else return s < W ? (uint32_t)Tw[b] : (uint32_t)ld_tab(Tg + b);
+            else return s < W ? (uint32_t)Tw[b] : (uint32_t)ld_row(Tg + b);
         } else if constexpr (!WIN) {
             return Fw[s];
         } else {
-            return s < W ? (uint32_t)Fw[s] : (uint32_t)ld_tab(Fg + s);
+            return s < W ? (uint32_t)Fw[s] : (uint32_t)ld_row(Fg + s);
         }
     }
 };
@@ -349,19 +396,89 @@ constexpr uint32_t kFBBytes = (1u << (2 * kFBK)) / 8;  // 4^K1 bits of shared me
 static __host__ __device__ constexpr uint32_t inv_buf_words(uint32_t slice_words) {  // uint16, 16-B multiple
     return (slice_words + 8 + 7) & ~7u;
 }
+#ifndef PFAC_JPRE
+#define PFAC_JPRE 0  // A/B knob: 1 = J2 prefetch at filter time in the 1024-position uint32 text kernels
+#endif
+#ifndef PFAC_JPRE_K
+#define PFAC_JPRE_K 8
+#endif
+#ifndef PFAC_JPRE_PROBE
+#define PFAC_JPRE_PROBE 0  // probe: the JPRE shared-memory buffer allocated, never used
+#endif
+constexpr uint32_t kJPreK = PFAC_JPRE_K;  // J2 prefetch slots per lane and 1024-position group
+static_assert(kK2Max + 7 <= 24, "JPRE: a lane's K2-mers come from its 64-bit text window (>= 24 bases)");
+// J2 prefetch (JPRE): the 1024-position-slice text kernels of uint32 images (large automata, ~9% of
+// positions flagged) have the shared memory for a per-lane buffer of kJPreK J2 entries
+static __host__ __device__ constexpr bool jpre_for(bool txt, uint32_t bm_words, uint32_t cell) {
+    return PFAC_JPRE && txt && bm_words == 32 && cell == 4;
+}
 static __host__ __device__ constexpr uint32_t warp_bytes(uint32_t slice_words, bool bar = false, bool txt = false,
-                                                         uint32_t bm_words = kBmWords) {
+                                                         uint32_t bm_words = kBmWords, bool jpre = false) {
     // TXT: ASCII staging (slice_words * 16 bytes) + ONE packed slice and barrier-bit buffer (the warp
     // packs a slice before it prefetches the next one's bytes, so the ASCII buffer is the double buffer)
     return txt ? slice_words * 16 + (slice_words + 4) * 4 + 16 + qcap_for(bm_words) * 2 + bm_words * 4 +
-                     inv_buf_words(slice_words) * 2
+                     inv_buf_words(slice_words) * 2 + (jpre ? 32 * kJPreK * 4 : 0)
                : 2 * (slice_words + 4) * 4 + 16 + qcap_for(bm_words) * 2 + bm_words * 4 +  // text, mbarriers, queue, bitmap
                      (bar ? 2 * inv_buf_words(slice_words) * 2 : 0);          // BAR: the slice's barrier bits
 }
 
+// Places one match-log record: cnt entries (offset in the slice, id) at ranks r0.. of the list, slice
+// positions from pbase.  128 entries per step, the next step's loads issued before this one's stores
+// (as in warp_stream): the replay is a stream, not a chain of load-use latencies.  The record was
+// written by this warp in this launch (coherent L2 loads).
+__device__ __forceinline__ void replay_record(const CompactArgs &c, const uint32_t *ent, uint32_t cnt, uint64_t r0,
+                                              uint64_t pbase, uint32_t lane) {
+    const uint32_t steps = (cnt + 127) / 128;
+    if (c.pid16) {
+        uint32_t e[4], en[4];
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) e[k] = lane + 32 * k < cnt ? __ldcg(ent + lane + 32 * k) : 0u;
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t i0 = st * 128 + lane;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) en[k] = i0 + 128 + 32 * k < cnt ? __ldcg(ent + i0 + 128 + 32 * k) : 0u;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                if (i0 + 32 * k < cnt) put_match(c, r0 + i0 + 32 * k, pbase + (e[k] & 0xFFFFu), e[k] >> 16);
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) e[k] = en[k];
+        }
+    } else {
+        const uint2 *ent2 = reinterpret_cast<const uint2 *>(ent);
+        uint2 e[4], en[4];
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) e[k] = lane + 32 * k < cnt ? __ldcg(ent2 + lane + 32 * k) : make_uint2(0, 0);
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t i0 = st * 128 + lane;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                en[k] = i0 + 128 + 32 * k < cnt ? __ldcg(ent2 + i0 + 128 + 32 * k) : make_uint2(0, 0);
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                if (i0 + 32 * k < cnt) put_match(c, r0 + i0 + 32 * k, pbase + e[k].x, e[k].y);
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) e[k] = en[k];
+        }
+    }
+}
+
+// Grid-wide barrier of a cooperative launch (every CTA resident) on a per-call zeroed counter.
+__device__ __forceinline__ void grid_sync(uint64_t *ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(reinterpret_cast<unsigned long long *>(ctr), 1ull);
+        while (ld_acquire_u64(ctr) < gridDim.x) __nanosleep(64);
+    }
+    __syncthreads();
+}
+
+constexpr uint32_t kSpillBit = 0x80000000u;  // DYN: a slice's count word, its matches not logged
+
 template <typename CT, bool WIN, int K, bool FUSE, bool FBM, bool BAR = false, bool LIST = false, bool TXT = false,
-          uint32_t SL = kSlice>
-__global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
+          uint32_t SL = kSlice, bool DYN = false>
+__global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p) {
+    constexpr int kMWarps = mt_for(SL) / 32;  // warps per CTA of this instantiation
     // positions per slice (text kernel for large automata: 1024, which leaves L1 more room)
     static_assert(SL % 1024 == 0 && SL <= 65536, "slice = whole 1024-position groups, u16 positions");
     constexpr uint32_t kSliceT = SL, kHalvesT = SL / 1024, kBmWordsT = SL / 32;
@@ -369,6 +486,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     static_assert(!BAR || FBM, "barrier semantics are implemented on the filter path");
     static_assert(!LIST || (FUSE && FBM), "list-only mode is the fused kernel on the filter path");
     static_assert(!TXT || (FUSE && BAR), "text mode is the fused kernel with per-slice barriers");
+    static_assert(!DYN || TXT, "dynamic slice claiming: the text kernel");
     constexpr uint32_t NJ = 1u << (2 * K);
     constexpr uint32_t MASK = NJ - 1;
     constexpr uint32_t ALIVE = sizeof(CT) == 2 ? 0x8000u : 0x80000000u;
@@ -380,7 +498,11 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     CT *sT = reinterpret_cast<CT *>(smem + (FBM ? kFBBytes : NJ * sizeof(CT)));
     CT *sF = sT + (size_t)p.window * kRowCells;
     uint8_t *wbase = reinterpret_cast<uint8_t *>(sF + (kMergedF ? 0 : p.window));  // 16-byte aligned (W % 8 == 0)
-    const uint32_t WB = warp_bytes(p.slice_words, BAR, TXT, kBmWordsT);
+    // JPRE: each flagged position's J2 entry is fetched (cp.async, LDGSTS) into a per-lane buffer as
+    // soon as the filter flags it; the drain reads it from shared memory, so the L2 latency of the
+    // first sub-slices' lookups hides behind the later sub-slices' filter work
+    constexpr bool JPRE = FBM && jpre_for(TXT, kBmWordsT, sizeof(CT)) && !PFAC_JPRE_PROBE;
+    const uint32_t WB = warp_bytes(p.slice_words, BAR, TXT, kBmWordsT, FBM && jpre_for(TXT, kBmWordsT, sizeof(CT)));
     uint64_t *tab_bar = reinterpret_cast<uint64_t *>(wbase + kMWarps * WB);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -392,6 +514,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     uint32_t *bm = reinterpret_cast<uint32_t *>(queue + kQCap);  // fused: nonzero cells of the slice
     uint16_t *inv0 = reinterpret_cast<uint16_t *>(bm + kBmWordsT);  // BAR: barrier bits of the slice
     uint16_t *inv1 = TXT ? inv0 : inv0 + inv_buf_words(p.slice_words);
+    uint32_t *jbuf = reinterpret_cast<uint32_t *>(inv1 + inv_buf_words(p.slice_words));  // JPRE: [32][kJPreK]
+    (void)jbuf;
     const uint32_t lt = (1u << lane) - 1;
     // grid_prefix's per-warp counts live in the dynamic region too: with no static shared memory the
     // dynamic region (FB first) starts right after the 1 KiB the system reserves, which the filter
@@ -413,7 +537,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     const uint64_t gw = (uint64_t)blockIdx.x * kMWarps + warp;
     // slice schedule: strided over the grid, or (fused) a contiguous run per warp so that the warp's
     // matches come out in position order
-    constexpr bool CONTIG = FUSE || kContiguousSchedule;
+    // DYN: warps claim slices from a global counter (walk-heavy text: per-slice work varies widely)
+    constexpr bool CONTIG = !DYN && (FUSE || kContiguousSchedule);
     // contiguous runs balanced to within one slice: warp gw owns [gw*N/TW, (gw+1)*N/TW) (a ceil-sized
     // run per warp would leave the last warps idle: cfg2 has 30.2 slices per warp)
 #if PFAC_BALANCED
@@ -475,7 +600,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             if (fb) bulk_g2s(sF, p.F, fb, tab_bar);
         }
     }
-    if (lane == 0 && s_first < s_end) issue(s_first, txt0, &bar[0]);
+    // DYN: the first slice, then each next one claimed one slice ahead (its TMA is issued mid-slice)
+    uint64_t sl0 = s_first, claim = 0;
+    if constexpr (DYN) {
+        if (lane == 0) claim = atomicAdd(reinterpret_cast<unsigned long long *>(p.c.ctl), 1ull);
+        sl0 = __shfl_sync(~0u, claim, 0);
+    }
+    if (lane == 0 && sl0 < s_end) issue(sl0, txt0, &bar[0]);
     const Tab<CT, WIN> tb{sT, sF, reinterpret_cast<const CT *>(p.T), reinterpret_cast<const CT *>(p.F), p.window};
     if constexpr (!TXT) mbar_wait(tab_bar, 0);  // TXT: after packing the first slice (overlaps the load)
     bool pred_bar = false;  // TXT: the previous slice had a barrier (FASTA text: every slice has one)
@@ -490,7 +621,13 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     bool bad_done = false;    // TXT: this warp has reported its first non-ACGT byte (slices ascend)
     uint64_t *spos = FUSE ? p.c.stage_pos + gw * p.c.stg : nullptr;
     uint32_t *spid = FUSE ? p.c.stage_pid + gw * p.c.stg : nullptr;
-    for (uint64_t sl = s_first; sl < s_end; sl += s_stride, ++it) {
+    uint64_t sl_next = 0;
+    for (uint64_t sl = sl0; sl < s_end; sl = sl_next, ++it) {
+        if constexpr (DYN) {
+            if (lane == 0) claim = atomicAdd(reinterpret_cast<unsigned long long *>(p.c.ctl), 1ull);
+        } else {
+            sl_next = sl + s_stride;
+        }
         const uint32_t buf = it & 1;
         if (!TXT && lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, buf ? txt0 : txt1, &bar[buf ^ 1]);
             if (FUSE) {
@@ -595,7 +732,8 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 }
             }
             __syncwarp();  // the ASCII buffer is free: fetch the next slice while this one is matched
-            if (lane == 0 && sl + s_stride < s_end) issue(sl + s_stride, txt0, &bar[0]);
+            if constexpr (DYN) sl_next = __shfl_sync(~0u, claim, 0);
+            if (lane == 0 && sl_next < s_end) issue(sl_next, txt0, &bar[0]);
             if (it == 0) mbar_wait(tab_bar, 0);
         } else if (BAR && !no_bar) {
             uint32_t any = 0;
@@ -628,10 +766,15 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 #pragma unroll
             for (uint32_t k = 0; k < kDrainIPL; ++k) {
                 const uint32_t i = lane + 32 * k;
-                dl[k] = i < take ? queue[qb + i] : 0xFFFFu;
+                const uint32_t e = i < take ? queue[qb + i] : 0xFFFFu;
+                // JPRE entries: bit 15 = J2 prefetched into slot (bits 12-14) of the owner lane's buffer
+                dl[k] = JPRE && i < take ? e & 0xFFFu : e;
                 dle[k] = (BAR && bar_slice && i < take) ? next_barrier(dl[k]) : lend;
-                dg[k] = (i < take && dl[k] + p.K2 <= dle[k]) ? ld_tab(p.J2 + (window16(txt, dl[k]) & p.mask2))
-                                                             : 0xFFFFFFFFu;
+                if (JPRE && i < take && (e & 0x8000u))
+                    dg[k] = jbuf[((dl[k] >> 3) & 31u) * kJPreK + ((e >> 12) & 7u)];
+                else
+                    dg[k] = (i < take && dl[k] + p.K2 <= dle[k]) ? ld_j2(p.J2 + (window16(txt, dl[k]) & p.mask2))
+                                                                 : 0xFFFFFFFFu;
             }
         };
         auto resolve = [&]() {
@@ -649,7 +792,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     if ((g & kJ2NB) && (le - l2 < kHRBases || ((window16(txt, l2) ^ (g >> kHRIndexBitsNB)) & 0xFFu)))
                         res = 0;
                     else
-                        res = walk_head(tb, txt, ld_tab(p.HR + (g & (g & kJ2NB ? (1u << kHRIndexBitsNB) - 1 : kJ2NB - 1))),
+                        res = walk_head(tb, txt, ld_j2(p.HR + (g & (g & kJ2NB ? (1u << kHRIndexBitsNB) - 1 : kJ2NB - 1))),
                                         l2, le);
                 }
                 else if (g & 0x80000000u) res = walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, le);
@@ -662,6 +805,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // Walk the queued positions (FBM: rounds as above) until at most `keep` remain.  The
         // __syncwarp orders the queue writes and the owners' v4 stores before these patch stores.
         auto drain = [&](uint32_t keep) {
+            if constexpr (JPRE) cp_async_wait_all();  // this lane's prefetches (the loop's __syncwarp: all lanes')
             while (qn > keep) {
                 __syncwarp();
                 if constexpr (FBM) {
@@ -708,7 +852,15 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         // Queue this lane's alive positions (bit r*8+j of `am` = position r*256 + lane*8 + j), one per
         // lane and round: a round costs one ballot, and there are max-over-lanes(popc(am)) rounds.
         // lg: log2 of the positions per lane per sub-slice of the bits in am (3: 8 positions, 4: 16)
-        auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3, bool defer = false) {
+        // pf (JPRE): the lane's flagged positions of this group had their J2 entries prefetched, the k-th
+        // (in bit order) into slot k of its buffer (k < kJPreK)
+        auto push = [&](uint32_t am, uint32_t gbase, uint32_t lg = 3, bool defer = false, bool pf = false) {
+            uint32_t kk = 0;
+            auto tag = [&]() -> uint32_t {
+                const uint32_t t = (JPRE && pf && kk < kJPreK) ? 0x8000u | (kk << 12) : 0u;  // (kJPreK <= 8)
+                ++kk;
+                return t;
+            };
             // The lanes' slots are the exclusive prefix of their counts c: from two ballots of the bits
             // of c when every c <= 3 (sparse groups: no shuffle chain), else a shuffle scan.  Each lane
             // then writes its own positions -- no ballot round per queued position.
@@ -737,7 +889,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint32_t bit = __ffs(am) - 1;
                     am &= am - 1;
                     queue[slot++] =
-                        (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
+                        (uint16_t)((gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1))) | tag());
                 }
                 qn += total;
                 finish(defer);
@@ -752,7 +904,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                     const uint32_t bit = __ffs(am) - 1;
                     am &= am - 1;
                     queue[qn + __popc(b & lt)] =
-                        (uint16_t)(gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1)));
+                        (uint16_t)((gbase + (bit >> lg) * (32u << lg) + (lane << lg) + (bit & ((1u << lg) - 1))) | tag());
                 }
                 qn += __popc(b);
             }
@@ -786,6 +938,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 #pragma unroll 1
           for (uint32_t hg = 0; hg < kHalvesT; ++hg) {
             uint32_t am = 0;
+            [[maybe_unused]] uint32_t kc = 0;  // JPRE: this lane's flagged positions so far in the group
 #pragma unroll kPh1Unroll
             for (uint32_t r = 0; r < 4; ++r) {
                 const uint32_t l0 = hg * 1024 + r * kSubN + lane * kP;
@@ -816,6 +969,14 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 #pragma unroll
                     for (uint32_t j = 0; j < kP; ++j)
                         m |= ((fb_word(x64, 2 * j) >> ((uint32_t)(x64 >> (2 * j)) & 31)) & 1u) << j;
+                    }
+                    if constexpr (JPRE) {  // the flagged positions' J2 entries (K2-mer at l0 + j, in x64)
+                        for (uint32_t mm = m; mm; mm &= mm - 1) {
+                            const uint32_t j = __ffs(mm) - 1;
+                            if (kc < kJPreK)
+                                cp_async4(jbuf + lane * kJPreK + kc, p.J2 + ((uint32_t)(x64 >> (2 * j)) & p.mask2));
+                            ++kc;
+                        }
                     }
                     if constexpr (!LIST) {  // the sub-slice's zeros: every store is zeros, so the warp
                         // writes two contiguous 512-B runs (A/B knob: each lane its own 8 positions)
@@ -849,7 +1010,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
                 }
             }
             resolve_pending();  // the previous group's round: its J2 loads had this filter step to land
-            push(am, hg * 1024, 3, FBM);
+            push(am, hg * 1024, 3, FBM, JPRE);
           }
           resolve_pending();
         } else if (BAR && bar_slice) {
@@ -964,10 +1125,21 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
 #pragma unroll
                 for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(~0u, cnt, d);
             }
+            if constexpr (DYN) {
+                // every slice's count (bit 31: spilled, placed by the owner of its chunk after the scan);
+                // a slice with matches is logged as [slice, count, entries] when the log has room
+                const uint32_t eb = p.c.pid16 ? 4u : 8u;
+                const uint32_t rec = log_record_bytes(cnt, eb);
+                const bool logged = cnt && kMatchLog && log_off + rec <= p.c.log_pw;
+                if (lane == 0) p.c.scnt[sl] = cnt | (cnt && !logged ? kSpillBit : 0u);
+                if (cnt && !logged && LIST)  // out[] is valid only at matches: keep the slice's bitmap
+                    for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = bm[w];
+                if (!logged) cnt = 0;  // nothing to log below
+            }
             if (!cnt) {  // after a spill, list-only mode still needs this slice's (empty) bitmap
-                if (LIST && spill_rel != ~0u)
+                if (!DYN && LIST && spill_rel != ~0u)
                     for (uint32_t w = lane; w < kBmWordsT; w += 32) p.c.bitmap[sl * kBmWordsT + w] = 0u;
-            } else if (wstaged == wcount && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
+            } else if (!DYN && wstaged == wcount && wcount + cnt <= p.c.stg) {  // (stg < 2^32)
 #pragma unroll 1
                 for (uint32_t w0 = 0; w0 < kBmWordsT; w0 += 32) {
                     uint32_t w = bm[w0 + lane];
@@ -993,14 +1165,14 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
             } else {
                 const uint32_t eb = p.c.pid16 ? 4u : 8u;
                 const uint32_t rec = log_record_bytes(cnt, eb);
-                if (kMatchLog && spill_rel == ~0u && log_off + rec <= p.c.log_pw) {
+                if (DYN || (kMatchLog && spill_rel == ~0u && log_off + rec <= p.c.log_pw)) {
                     // the staging is full: log the slice -- header [slice (relative), count], then
                     // (offset, pid) per match in position order -- to be placed after the prefix by a
                     // coalesced copy instead of re-reading out[]
                     uint32_t *hdr = reinterpret_cast<uint32_t *>(p.c.log + gw * p.c.log_pw + log_off);
                     uint32_t *ent = hdr + 4;
                     if (lane == 0) {
-                        hdr[0] = (uint32_t)(sl - s_first);
+                        hdr[0] = (uint32_t)(DYN ? sl : sl - s_first);  // DYN: the absolute slice
                         hdr[1] = cnt;
                     }
                     // 128 positions per step: lane t owns positions 4t..4t+3 (one 16-byte read of the
@@ -1054,7 +1226,47 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
     // TXT: a warp that had no slice never waited for the table copy; no CTA may retire while its
     // bulk copy into shared memory is in flight
     if (TXT && it == 0) mbar_wait(tab_bar, 0);
-    if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
+    if constexpr (DYN) {
+        // every slice is matched: scan the per-slice counts (a contiguous chunk of slices per warp, the
+        // warps' chunk totals by grid_prefix), then replay this warp's log records at their slices'
+        // offsets; the spilled slices of each chunk are re-read from out[] by the chunk's warp
+        grid_sync(p.c.ctl + 1);
+        const uint64_t C = (p.nslices + TW - 1) / TW, lo = gw * C < p.nslices ? gw * C : p.nslices,
+                       hi = lo + C < p.nslices ? lo + C : p.nslices;
+        uint64_t sum = 0;
+        for (uint64_t s = lo + lane; s < hi; s += 32) sum += p.c.scnt[s] & ~kSpillBit;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(~0u, sum, d);
+        uint64_t run = grid_prefix<kMWarps>(sum, p.c.counts, p.c.d_count, s_wcount, s_woff);
+        for (uint64_t s0 = lo; s0 < hi; s0 += 32) {
+            const uint64_t s = s0 + lane;
+            const uint32_t c = s < hi ? p.c.scnt[s] & ~kSpillBit : 0u;
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(~0u, incl, d);
+                if (lane >= (uint32_t)d) incl += y;
+            }
+            if (s < hi) p.c.soff[s] = run + incl - c;
+            run += __shfl_sync(~0u, incl, 31);
+        }
+        grid_sync(p.c.ctl + 2);
+        for (uint32_t off = 0; kMatchLog && off < log_off;) {
+            const uint32_t *hdr = reinterpret_cast<const uint32_t *>(p.c.log + gw * p.c.log_pw + off);
+            const uint32_t s = __ldcg(hdr), cnt = __ldcg(hdr + 1);
+            replay_record(p.c, hdr + 4, cnt, __ldcg(p.c.soff + s), p.c.pos_base + (uint64_t)s * kSliceT, lane);
+            off += log_record_bytes(cnt, p.c.pid16 ? 4u : 8u);
+        }
+        for (uint64_t s = lo; s < hi; ++s) {
+            const uint32_t c = __ldcg(p.c.scnt + s);
+            if (!(c & kSpillBit)) continue;
+            const uint64_t a = s * kSliceT, b = a + kSliceT < p.n_own ? a + kSliceT : p.n_own;
+            warp_stream<false>(
+                p.c, a, b, __ldcg(p.c.soff + s),
+                [&](uint64_t rr, uint64_t i, uint32_t val) { put_match(p.c, rr, p.c.pos_base + i, val); },
+                LIST ? p.c.bitmap : nullptr);
+        }
+    } else if (FUSE) {  // grid-wide placement of the staged lists (cooperative launch: all CTAs resident)
         const uint64_t prefix = grid_prefix<kMWarps>(wcount, p.c.counts, p.c.d_count, s_wcount, s_woff);
         for (uint64_t i = lane; i < wstaged; i += 32) put_match(p.c, prefix + i, spos[i], spid[i]);
         // logged slices, in slice order: positions from each record's bitmap, pids from its list
@@ -1063,43 +1275,7 @@ __global__ void __launch_bounds__(kMT, 1) match_kernel(const MatchArgs p) {
         for (uint32_t off = 0; kMatchLog && off < log_off;) {
             const uint32_t *hdr = reinterpret_cast<const uint32_t *>(p.c.log + gw * p.c.log_pw + off);
             const uint32_t rel = __ldcg(hdr), cnt = __ldcg(hdr + 1);  // this warp's own log (coherent L2 loads)
-            const uint32_t *ent = hdr + 4;
-            const uint64_t pbase = p.c.pos_base + (s_first + rel) * kSliceT;
-            // 128 entries per step, the next step's loads issued before this one's stores (as in
-            // warp_stream): the replay is a stream, not a chain of load-use latencies
-            const uint32_t steps = (cnt + 127) / 128;
-            if (p.c.pid16) {
-                uint32_t e[4], en[4];
-#pragma unroll
-                for (uint32_t k = 0; k < 4; ++k) e[k] = lane + 32 * k < cnt ? __ldcg(ent + lane + 32 * k) : 0u;
-                for (uint32_t st = 0; st < steps; ++st) {
-                    const uint32_t i0 = st * 128 + lane;
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k)
-                        en[k] = i0 + 128 + 32 * k < cnt ? __ldcg(ent + i0 + 128 + 32 * k) : 0u;
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k)
-                        if (i0 + 32 * k < cnt) put_match(p.c, r0 + i0 + 32 * k, pbase + (e[k] & 0xFFFFu), e[k] >> 16);
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) e[k] = en[k];
-                }
-            } else {
-                const uint2 *ent2 = reinterpret_cast<const uint2 *>(ent);
-                uint2 e[4], en[4];
-#pragma unroll
-                for (uint32_t k = 0; k < 4; ++k) e[k] = lane + 32 * k < cnt ? __ldcg(ent2 + lane + 32 * k) : make_uint2(0, 0);
-                for (uint32_t st = 0; st < steps; ++st) {
-                    const uint32_t i0 = st * 128 + lane;
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k)
-                        en[k] = i0 + 128 + 32 * k < cnt ? __ldcg(ent2 + i0 + 128 + 32 * k) : make_uint2(0, 0);
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k)
-                        if (i0 + 32 * k < cnt) put_match(p.c, r0 + i0 + 32 * k, pbase + e[k].x, e[k].y);
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) e[k] = en[k];
-                }
-            }
+            replay_record(p.c, hdr + 4, cnt, r0, p.c.pos_base + (s_first + rel) * kSliceT, lane);
             r0 += cnt;
             off += log_record_bytes(cnt, p.c.pid16 ? 4u : 8u);
         }
@@ -1148,9 +1324,10 @@ constexpr uint32_t kTxtMaxRows = PFAC_TXT_MAX_ROWS;  // larger automata: the tex
 constexpr uint32_t kSliceSmall = 1024;  // the fused kernel's static shared arrays (grid_prefix)
 
 static size_t match_smem(size_t table_bytes, uint32_t cell, uint32_t window, uint32_t slice_words,
-                         bool bar = false, bool txt = false, uint32_t bm_words = kBmWords) {
-    return table_bytes + (size_t)window * kWinCells * cell + (size_t)kMWarps * warp_bytes(slice_words, bar, txt, bm_words) +
-           16 + 2 * kMWarps * 8;  // + the table mbarrier and grid_prefix's per-warp counts
+                         bool bar = false, bool txt = false, uint32_t bm_words = kBmWords, bool jpre = false) {
+    const size_t nw = (size_t)mt_for(bm_words * 32) / 32;
+    return table_bytes + (size_t)window * kWinCells * cell + nw * warp_bytes(slice_words, bar, txt, bm_words, jpre) +
+           16 + 2 * nw * 8;  // + the table mbarrier and grid_prefix's per-warp counts
 }
 
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
@@ -1206,7 +1383,8 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
     // the rows of large automata (cfg4: 1.84 vs 2.16 ms for 2048-position slices, vs 1.92 for pack +
     // fused); 2% slower on cfg2-like automata, so it serves only those the 2048 plan is not used for
     pl.slice_words_1k = kSliceSmall / 16 + halo_words_for(h.K2 > h.K ? h.K2 : h.K, maxlen);
-    const size_t fixed_k = match_smem(table, pl.cell, 0, pl.slice_words_1k, true, true, kSliceSmall / 32) +
+    const bool jpre = jpre_for(true, kSliceSmall / 32, pl.cell);
+    const size_t fixed_k = match_smem(table, pl.cell, 0, pl.slice_words_1k, true, true, kSliceSmall / 32, jpre) +
                            kStaticSmemReserve;
     pl.txt1k_ok = h.K2 != 0 && (size_t)optin >= fixed_k;
     uint32_t wk = pl.txt1k_ok ? (uint32_t)(((size_t)optin - fixed_k) / (kWinCells * pl.cell)) & ~7u : 0u;
@@ -1216,7 +1394,7 @@ MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen) {
 #endif
     pl.all_smem_txt1k = wk >= h.rows;
     pl.window_txt1k = pl.all_smem_txt1k ? h.rows : wk;
-    pl.smem_txt1k = match_smem(table, pl.cell, pl.window_txt1k, pl.slice_words_1k, true, true, kSliceSmall / 32);
+    pl.smem_txt1k = match_smem(table, pl.cell, pl.window_txt1k, pl.slice_words_1k, true, true, kSliceSmall / 32, jpre);
     pl.txt1k_pref = pl.txt1k_ok && !pl.txt_pref && pl.txt_ok && h.rows > kTxtMaxRows;
     pl.sms = sms;
     return pl;
@@ -1251,17 +1429,24 @@ static void fill_args(MatchArgs &a, const DeviceImage &img, const uint32_t *d_pa
     a.HR = reinterpret_cast<const uint4 *>(img.d_HR);
 }
 
-template <typename CT, bool LIST, uint32_t SL = kSlice>
+template <typename CT, bool LIST, uint32_t SL = kSlice, bool DYN = false>
 static const void *txt_kernel(bool all_smem) {
-    return all_smem ? (const void *)match_kernel<CT, false, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL>
-                    : (const void *)match_kernel<CT, true, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL>;
+    return all_smem ? (const void *)match_kernel<CT, false, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL, DYN>
+                    : (const void *)match_kernel<CT, true, sizeof(CT) == 2 ? kJumpK16 : kJumpK32, true, true, true, LIST, true, SL, DYN>;
 }
 
 template <bool FUSE>
 static const void *kernel_for(const DeviceImage &img, bool bar, bool list = false, bool txt = false,
-                              bool small = false) {
+                              bool small = false, bool dyn = false) {
     const MatchPlan &pl = img.plan;
     if constexpr (FUSE) {
+        if (txt && small && dyn) {  // text input, 1024-position slices claimed dynamically
+            if (pl.cell == 2)
+                return list ? txt_kernel<uint16_t, true, kSliceSmall, true>(pl.all_smem_txt1k)
+                            : txt_kernel<uint16_t, false, kSliceSmall, true>(pl.all_smem_txt1k);
+            return list ? txt_kernel<uint32_t, true, kSliceSmall, true>(pl.all_smem_txt1k)
+                        : txt_kernel<uint32_t, false, kSliceSmall, true>(pl.all_smem_txt1k);
+        }
         if (txt && small) {  // text input, 1024-position slices
             if (pl.cell == 2)
                 return list ? txt_kernel<uint16_t, true, kSliceSmall>(pl.all_smem_txt1k)
@@ -1314,7 +1499,7 @@ static int launch(const DeviceImage &img, const void *fn, uint64_t grid, MatchAr
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kMT);
+    cfg.blockDim = dim3(small ? mt_for(kSliceSmall) : kMT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -1359,8 +1544,9 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint64_t n_own, uint64_t n_avail, int32_t *d_out, uint64_t pos_base, uint64_t *d_pos,
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only, const uint8_t *d_text, uint64_t *d_first_bad,
-                         const uint64_t *d_bad_all, bool small) {
+                         const uint64_t *d_bad_all, bool small, bool dyn) {
     small = small && d_text;  // 1024-position slices: the text kernel only
+    dyn = dyn && small;       // dynamic slice claiming: its 1024-position form only
     cudaStream_t st = (cudaStream_t)stream;
     if (d_first_bad && (d_text || n_own == 0)) {
         cudaError_t e = cudaMemsetAsync(d_first_bad, 0xFF, 8, st);
@@ -1378,7 +1564,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     a.bad_all = d_text ? nullptr : d_bad_all;
     const MatchPlan &pl = img.plan;
     const uint64_t grid = (uint64_t)pl.sms < a.nslices ? (uint64_t)pl.sms : a.nslices;
-    const uint64_t warps = grid * kMWarps;
+    const uint64_t warps = grid * (uint64_t)(mt_for(slice) / 32);
     a.slices_per_warp = (a.nslices + warps - 1) / warps + PFAC_SPW_PAD;
     CompactArgs &c = a.c;
     c.out = d_out;
@@ -1401,10 +1587,15 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.log_pw = kMatchLog ? (match_log_bytes(n_own) / warps) & ~15ull : 0;
     c.pid16 = k < 65536u;
     c.chunk = a.slices_per_warp * slice;
-    cudaError_t e = cudaMemsetAsync(c.counts, 0, (size_t)grid * 8, st);
+    // DYN: the per-slice counts and offsets in the staging area (nslices * 12 <= its 12 B per entry),
+    // the claim counter and the two grid barriers at the end of the CTA-count array
+    c.soff = c.stage_pos;
+    c.scnt = reinterpret_cast<uint32_t *>(c.soff + a.nslices);
+    c.ctl = c.counts + kGMax - 4;
+    cudaError_t e = cudaMemsetAsync(c.counts, 0, dyn ? (size_t)kGMax * 8 : (size_t)grid * 8, st);
     if (e != cudaSuccess) return e;
-    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr, small), grid, a, true,
-                  st, small);
+    return launch(img, kernel_for<true>(img, d_inv != nullptr, list_only, d_text != nullptr, small, dyn), grid, a,
+                  true, st, small);
 }
 
 }  // namespace pfac

@@ -199,7 +199,7 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
                          uint32_t *d_pid, uint64_t capacity, uint64_t *d_count, uint64_t *d_hist, void *d_workspace,
                          void *stream, bool list_only = false, const uint8_t *d_text = nullptr,
                          uint64_t *d_first_bad = nullptr, const uint64_t *d_bad_all = nullptr,
-                         bool small = false);
+                         bool small = false, bool dyn = false);
 MatchPlan plan_match(int device, const HostImage &h, uint32_t maxlen);
 int launch_expand(const DeviceImage &img, uint32_t k, const uint64_t *d_pos, const uint32_t *d_pid,
                   const uint64_t *d_count, uint64_t in_capacity, uint64_t *d_pos_all, uint32_t *d_pid_all,

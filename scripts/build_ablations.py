@@ -30,6 +30,15 @@ VARIANTS = {
     "chain16": ["PFAC_CHAIN32=0"],           # A/B: 16 forced bases per uint32 chain row (round 1)
     "noend": ["PFAC_ENDDEAD=0"],             # A/B: no end-state answers in uint32 chain rows
     "fb_add": ["PFAC_FB_LOP=0"],             # A/B: filter word addresses as base + offset (one more IADD per lookup)
+    "jpre_probe": ["PFAC_JPRE=1", "PFAC_JPRE_PROBE=1"],     # probe: the J2 prefetch buffer allocated (shared memory), not used
+    "jpre4": ["PFAC_JPRE=1", "PFAC_JPRE_K=4"],              # A/B: 4 J2 prefetch slots per lane
+    "jpre": ["PFAC_JPRE=1"],                 # A/B: J2 prefetch (cp.async at filter time) in the 1024-position uint32 text kernels
+    "j2na": ["PFAC_J2_NA=1"],                # A/B: J2 and HR loads ld.global.nc.L1::no_allocate
+    "tabna": ["PFAC_TAB_NA=1"],              # A/B: every table load L1::no_allocate
+    "mt1k": ["PFAC_MT_1K=1024"],             # A/B: 32 warps per CTA in the 1024-position-slice text kernels
+    "mt1k640": ["PFAC_MT_1K=640"],           # A/B: 20 warps per CTA in the 1024-position-slice text kernels
+    "mt1k512": ["PFAC_MT_1K=512"],           # A/B: 16 warps per CTA (shared memory under the 164-KB carve-out: more L1)
+    "nojpre": ["PFAC_JPRE=0"],               # A/B: no J2 prefetch (cp.async at filter time) in the 1024-position uint32 text kernels
 }
 
 if __name__ == "__main__":

@@ -200,13 +200,14 @@ def test_text_walk_stats_closed_forms():
 
 def test_plan_text_policy():
     """pfac_plan_text: walk-heavy text (repetitive text against cfg5's nested families: ~20% of walks
-    make >= 16 transitions) gets the 1024-position-slice text kernel; random text keeps the plan."""
+    make >= 16 transitions) gets the 1024-position-slice text kernel with dynamically claimed slices
+    (mode 3); random text keeps the plan."""
     cfg = gen.CONFIGS[5]
     p5 = gen.config_patterns(cfg)
     a = Automaton(p5)
     rep = gen.config_text(cfg, 0, 400_000, patterns=p5, n=cfg.n)
     mode, deep = a.plan_text(rep, stride=3)
-    assert mode == 2 and deep > 0.05
+    assert mode == 3 and deep > 0.05
     rnd = gen.iid_text(9, 0, 400_000)
     mode, deep = a.plan_text(rnd, stride=3)
     assert mode == -1 and deep < 0.01

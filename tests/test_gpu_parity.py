@@ -281,7 +281,7 @@ def _full_config(idx):
     del packed, ws
     # the text-input call (pack fused into the kernel; the bench default where the plan takes it) in
     # both of its paths, on the same full input: list, count, first_bad and the whole dense out[]
-    for mode in (1, 0, 2):
+    for mode in (1, 0, 2, 3):
         a.set_text_kernel(mode)
         ws = torch.empty(P.match_text_workspace_bytes(n, n), dtype=torch.uint8, device=DEV)
         out3 = torch.empty(n, dtype=torch.int32, device=DEV)
@@ -451,7 +451,7 @@ def test_config2_fasta_full_text_kernel():
     epos, epid = _oracle_list_parallel(pats, text)
     bad_idx = int(np.nonzero(~np.isin(text[:1000], np.frombuffer(b"ACGTacgt", np.uint8)))[0][0])
     o = Oracle(pats)
-    for mode in (1, 0):
+    for mode in (1, 0, 3):
         a.set_text_kernel(mode)
         out = torch.empty(n, dtype=torch.int32, device=DEV)
         cap = len(epos) + 1024
@@ -484,7 +484,7 @@ def test_text_beyond_2pow32_positions():
     epos, epid = _oracle_list_parallel(pats, text)
     assert len(epos) > 1_000_000 and int(epos[-1]) > (1 << 32)
     o = Oracle(pats)
-    for mode in (1, 0):
+    for mode in (1, 0, 3):
         a.set_text_kernel(mode)
         out = torch.empty(n, dtype=torch.int32, device=DEV)
         cap = len(epos) + 1024

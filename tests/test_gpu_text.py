@@ -27,11 +27,12 @@ ACGT8 = np.frombuffer(b"ACGTacgt", np.uint8)
 U64MAX = (1 << 64) - 1
 
 
-@pytest.fixture(autouse=True, params=["1", "0", "2"], ids=["one-kernel", "two-kernel", "one-kernel-1k"])
+@pytest.fixture(autouse=True, params=["1", "0", "2", "3"], ids=["one-kernel", "two-kernel", "one-kernel-1k",
+                                                              "one-kernel-1k-dyn"])
 def text_kernel(request, monkeypatch):
     """Both paths of pfac_match_text_async: the one-kernel TXT instantiation and the pack + fused
     kernel path the call takes for unaligned text or automata the policy keeps off TXT; "2": the text
-    kernel with 1024-position slices (both cell widths)."""
+    kernel with 1024-position slices (both cell widths); "3": that kernel with dynamically claimed slices."""
     monkeypatch.setattr(P.binding, "DEFAULT_TEXT_KERNEL", int(request.param))
     return request.param
 
@@ -187,9 +188,9 @@ def test_text_policy_info(text_kernel):
     """The image reports which path the call takes (pfac_image_info.text_kernel)."""
     a = P.Automaton(SETS["cfg2like"]())
     info = a.image_info(0)
-    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 2}[text_kernel]  # uint16 image
+    assert info["text_kernel"] == {"1": 1, "0": 0, "2": 2, "3": 3}[text_kernel]  # uint16 image
     b = P.Automaton(SETS["big32"]())  # uint32 image
-    assert b.image_info(0)["text_kernel"] == {"1": 1, "0": 0, "2": 2}[text_kernel]
+    assert b.image_info(0)["text_kernel"] == {"1": 1, "0": 0, "2": 2, "3": 3}[text_kernel]
     b.set_text_kernel(-1)  # back to the plan: a uint32 image with < 2^20 rows takes 2048-slice text
     assert b.image_info(0)["text_kernel"] in (1, 2)
 
