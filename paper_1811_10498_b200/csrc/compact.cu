@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(kCT) compact_kernel(const CompactArgs a) {
 
 // [counts kGMax | staging pos | staging pid | spilled slice bitmaps (fused kernel) | match logs (fused kernel)]
 uint64_t compact_workspace_bytes(uint64_t n) {
-    return (uint64_t)kGMax * 8 + ((stage_entries(n) * 12 + 15) & ~15ull) + spill_bitmap_bytes(n) + match_log_bytes(n);
+    return (uint64_t)kGMax * 8 + ((stage_entries(n) * 12 + 15) & ~15ull) + spill_bitmap_bytes(n) + match_log_bytes(n) +
+           dyn_area_bytes(n);
 }
 
 int launch_compact(const int32_t *d_out, uint64_t n, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,

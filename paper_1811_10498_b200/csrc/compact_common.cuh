@@ -167,6 +167,10 @@ __host__ __device__ constexpr uint32_t log_record_bytes(uint32_t cnt, uint32_t e
     return (16 + cnt * entry_bytes + 15) & ~15u;
 }
 
+// The dynamic-slice text kernel's per-slice arrays (1024-position slices): list offset (8 B) and
+// count word (4 B) per slice, after the match logs.
+inline uint64_t dyn_area_bytes(uint64_t n) { return (((n + 1023) / 1024) * 12 + 15) & ~15ull; }
+
 inline uint64_t stage_entries(uint64_t n) {
     const uint64_t cap = kStageBytes / 12;
     return n < cap ? n : cap;

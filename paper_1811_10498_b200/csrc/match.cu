@@ -1587,9 +1587,9 @@ int launch_match_compact(const DeviceImage &img, uint32_t k, const uint32_t *d_p
     c.log_pw = kMatchLog ? (match_log_bytes(n_own) / warps) & ~15ull : 0;
     c.pid16 = k < 65536u;
     c.chunk = a.slices_per_warp * slice;
-    // DYN: the per-slice counts and offsets in the staging area (nslices * 12 <= its 12 B per entry),
-    // the claim counter and the two grid barriers at the end of the CTA-count array
-    c.soff = c.stage_pos;
+    // DYN: the per-slice offsets and counts after the logs (dyn_area_bytes), the claim counter and the
+    // two grid barriers at the end of the CTA-count array
+    c.soff = reinterpret_cast<uint64_t *>(c.log + match_log_bytes(n_own));
     c.scnt = reinterpret_cast<uint32_t *>(c.soff + a.nslices);
     c.ctl = c.counts + kGMax - 4;
     cudaError_t e = cudaMemsetAsync(c.counts, 0, dyn ? (size_t)kGMax * 8 : (size_t)grid * 8, st);
