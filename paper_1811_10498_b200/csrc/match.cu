@@ -56,7 +56,7 @@ namespace pfac {
 #define PFAC_PH1_UNROLL 1
 #endif
 #ifndef PFAC_MT_1K
-#define PFAC_MT_1K PFAC_MT
+#define PFAC_MT_1K 1024  // the 1024-position text kernels: 32 warps (cfg4 -3.5%, cfg5 -4.4% vs 28; profiles/r02_cta_ab.jsonl)
 #endif
 constexpr int kMT = PFAC_MT;                // threads per CTA (A/B knob)
 constexpr int kPh1Unroll = PFAC_PH1_UNROLL; // sub-slices unrolled in the lookup phase (A/B knob)
@@ -374,8 +374,12 @@ static __host__ __device__ constexpr uint32_t drain_ipl_for(uint32_t bm_words) {
 }
 // queue of flagged positions (entries per warp): the 1024-position-slice kernels (large automata,
 // ~9% of positions flagged: ~90 per 1024-position group) have the shared memory for a longer one
+#ifndef PFAC_QEXTRA_1K
+#define PFAC_QEXTRA_1K 96  // queue beyond one drain round (1024-position kernels): keeps 32 warps' shared
+                           // memory under the 196-KB carve-out on uint32 images (more L1 for the misses)
+#endif
 static __host__ __device__ constexpr uint32_t qcap_for(uint32_t bm_words) {
-    return 32 * drain_ipl_for(bm_words) + (bm_words <= 32 ? 160 : 64);
+    return 32 * drain_ipl_for(bm_words) + (bm_words <= 32 ? PFAC_QEXTRA_1K : 64);
 }
 #ifndef PFAC_PUSH_SCAN
 #define PFAC_PUSH_SCAN 1  // A/B knob: 0 = one ballot round per queued position per lane
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p)
         // A drain round: issue() takes up to 32 * kDrainIPL queued items (kDrainIPL per lane) and issues
         // all their J2 loads; resolve() consumes them (an NB check, a chain-head row, a walk) and
         // patches out[].  One L2 round trip serves the whole round.
-        uint32_t dl[kDrainIPL], dg[kDrainIPL], dle[kDrainIPL];  // position, J2 entry, walk bound (barrier)
+        uint32_t dl[kDrainIPL], dg[kDrainIPL];  // position, J2 entry (the walk bound is recomputed: registers)
         auto issue = [&](uint32_t take, uint32_t qb) {
 #pragma unroll
             for (uint32_t k = 0; k < kDrainIPL; ++k) {
@@ -769,19 +773,20 @@ __global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p)
                 const uint32_t e = i < take ? queue[qb + i] : 0xFFFFu;
                 // JPRE entries: bit 15 = J2 prefetched into slot (bits 12-14) of the owner lane's buffer
                 dl[k] = JPRE && i < take ? e & 0xFFFu : e;
-                dle[k] = (BAR && bar_slice && i < take) ? next_barrier(dl[k]) : lend;
+                const uint32_t le = (BAR && bar_slice && i < take) ? next_barrier(dl[k]) : lend;
                 if (JPRE && i < take && (e & 0x8000u))
                     dg[k] = jbuf[((dl[k] >> 3) & 31u) * kJPreK + ((e >> 12) & 7u)];
                 else
-                    dg[k] = (i < take && dl[k] + p.K2 <= dle[k]) ? ld_j2(p.J2 + (window16(txt, dl[k]) & p.mask2))
-                                                                 : 0xFFFFFFFFu;
+                    dg[k] = (i < take && dl[k] + p.K2 <= le) ? ld_j2(p.J2 + (window16(txt, dl[k]) & p.mask2))
+                                                             : 0xFFFFFFFFu;
             }
         };
         auto resolve = [&]() {
 #pragma unroll
             for (uint32_t k = 0; k < kDrainIPL; ++k) {
-                const uint32_t l = dl[k], g = dg[k], le = dle[k];
+                const uint32_t l = dl[k], g = dg[k];
                 if (l == 0xFFFFu) continue;
+                const uint32_t le = (BAR && bar_slice) ? next_barrier(l) : lend;  // the walk's bound
                 uint32_t res;
                 if (g == 0xFFFFFFFFu) res = walk(tb, txt, p.root, l, le);  // near the end / a barrier
                 else if (sizeof(CT) == 4 && p.HR && (g & kJ2HR)) {  // a chain head's row copy
