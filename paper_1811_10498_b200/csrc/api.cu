@@ -418,9 +418,10 @@ int pfac_match_list_async(const pfac_automaton *a, const uint32_t *d_packed, con
 static uint64_t al16(uint64_t x) { return (x + 15) & ~15ull; }
 
 // Which path pfac_match_text_async runs for this image: 0 = pack -> fused kernel, 1 = the text kernel,
-// 2 = the text kernel with 1024-position slices, 3 = that kernel with slices claimed dynamically.  The plan's measured preference (MatchPlan::txt_pref,
-// txt1k_pref), unless pfac_set_text_kernel forced 0 (never) / 1 (whenever one fits; 2048 slices
-// first) / 2 (1024 slices whenever they fit).
+// 2 = the text kernel with 1024-position slices, 3 = that kernel with slices claimed dynamically.
+// The plan's measured preference (MatchPlan::txt_pref, txt1k_pref), unless pfac_set_text_kernel (or
+// pfac_plan_text) forced 0 (never) / 1 (whenever one fits; 2048 slices first) / 2 or 3 (1024 slices
+// whenever they fit).
 static int text_kernel_for(const pfac_automaton *a, const DeviceImage &im) {
     const int force = a->text_kernel.load(std::memory_order_relaxed);
     const MatchPlan &pl = im.plan;
