@@ -184,10 +184,37 @@ __device__ __forceinline__ T ld_j2(const T *p) {  // J2 entries and chain-head r
     else return ld_tab(p);
 }
 
+// Shared-window loads by 32-bit shared address (the row window is read through these, so the walk
+// loop does not convert a generic pointer to a shared address, an S2R, per step)
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_cell(uint32_t a, uint16_t) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_cell(uint32_t a, uint32_t) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+#ifndef PFAC_LDS_ADDR
+#define PFAC_LDS_ADDR 1  // A/B knob: 0 = the row window read through generic pointers
+#endif
+
 template <typename CT, bool WIN>
 struct Tab {
     const CT *Tw, *Fw, *Tg, *Fg;
     uint32_t W;
+    uint32_t sTa, sFa;  // shared-window addresses of Tw and Fw
     __device__ __forceinline__ Row<CT> row(uint32_t s) const {
         Row<CT> r;
         if constexpr (sizeof(CT) == 2 && kMergedF) {  // one 16-byte row: 4 transitions, F, padding
@@ -196,10 +223,10 @@ struct Tab {
             r.r = make_uint2(v.x, v.y);
             r.f = v.z & 0xFFFFu;
         } else if constexpr (sizeof(CT) == 2) {
-            if (!WIN || s < W) r.r = *reinterpret_cast<const uint2 *>(Tw + (size_t)s * kRowCells);
+            if (!WIN || s < W) r.r = PFAC_LDS_ADDR ? lds_v2(sTa + s * (kRowCells * 2)) : *reinterpret_cast<const uint2 *>(Tw + (size_t)s * kRowCells);
             else r.r = ld_row(reinterpret_cast<const uint2 *>(Tg + (size_t)s * kRowCells));
         } else {
-            if (!WIN || s < W) r.r = *reinterpret_cast<const uint4 *>(Tw + (size_t)s * kRowCells);
+            if (!WIN || s < W) r.r = PFAC_LDS_ADDR ? lds_v4(sTa + s * (kRowCells * 4)) : *reinterpret_cast<const uint4 *>(Tw + (size_t)s * kRowCells);
             else r.r = ld_row(reinterpret_cast<const uint4 *>(Tg + (size_t)s * kRowCells));
             if constexpr (kMergedF)
                 r.f = (!WIN || s < W) ? (uint32_t)Tw[(size_t)s * kRowCells + 4] : (uint32_t)ld_row(Tg + (size_t)s * kRowCells + 4);
@@ -212,9 +239,10 @@ struct Tab {
             if constexpr (!WIN) return Tw[b];
             else return s < W ? (uint32_t)Tw[b] : (uint32_t)ld_row(Tg + b);
         } else if constexpr (!WIN) {
-            return Fw[s];
+            return PFAC_LDS_ADDR ? lds_cell(sFa + s * (uint32_t)sizeof(CT), CT{}) : (uint32_t)Fw[s];
         } else {
-            return s < W ? (uint32_t)Fw[s] : (uint32_t)ld_row(Fg + s);
+            return s < W ? (PFAC_LDS_ADDR ? lds_cell(sFa + s * (uint32_t)sizeof(CT), CT{}) : (uint32_t)Fw[s])
+                         : (uint32_t)ld_row(Fg + s);
         }
     }
 };
@@ -236,6 +264,7 @@ __device__ __forceinline__ uint32_t nibble_rank(uint32_t m, uint32_t lt, uint32_
 // checked by plan_match).
 constexpr uint32_t kFBSmemBase = 1024;
 constexpr bool kFbLop = PFAC_FB_LOP && kFilterK == 10;  // the 0x1FFFC mask is FB's 128 KiB
+constexpr bool kLdsConst = PFAC_LDS_ADDR && kFbLop;  // row window at constant shared addresses
 
 bool fb_addressing_ok(int device) {
     int reserved = -1;
@@ -529,6 +558,7 @@ __global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p)
     if constexpr (kFbLop) {
         const uint32_t fb_sa = (uint32_t)__cvta_generic_to_shared(smem);
         if ((fb_sa & 0x1FFFFu) != kFBSmemBase) __trap();  // host-checked (fb_addressing_ok); never taken
+        if (kLdsConst && (fb_sa & ~0x1FFFFu) != 0) __trap();  // a non-cluster launch: CTA window high bits 0
         fb_hi = fb_sa & ~0x1FFFFu;
     }
     // the filter word of K1-mer bits [sh, sh + 2 K1) of x: bit (x >> sh) & 31 of word (x >> (sh + 5))
@@ -611,7 +641,13 @@ __global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p)
         sl0 = __shfl_sync(~0u, claim, 0);
     }
     if (lane == 0 && sl0 < s_end) issue(sl0, txt0, &bar[0]);
-    const Tab<CT, WIN> tb{sT, sF, reinterpret_cast<const CT *>(p.T), reinterpret_cast<const CT *>(p.F), p.window};
+    // the row window's shared-window address as a constant (+ the window size from the parameters):
+    // the dynamic region starts at kFBSmemBase of a CTA window whose high bits are 0 (checked above),
+    // so no walk step converts a generic pointer (an S2R the compiler would otherwise rematerialize)
+    constexpr uint32_t kTOff = kFBSmemBase + (FBM ? kFBBytes : NJ * (uint32_t)sizeof(CT));
+    const uint32_t sTa = kLdsConst ? kTOff : (uint32_t)__cvta_generic_to_shared(sT);
+    const Tab<CT, WIN> tb{sT, sF, reinterpret_cast<const CT *>(p.T), reinterpret_cast<const CT *>(p.F), p.window,
+                          sTa, sTa + p.window * (uint32_t)(kRowCells * sizeof(CT))};
     if constexpr (!TXT) mbar_wait(tab_bar, 0);  // TXT: after packing the first slice (overlaps the load)
     bool pred_bar = false;  // TXT: the previous slice had a barrier (FASTA text: every slice has one)
 
