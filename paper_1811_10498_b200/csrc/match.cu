@@ -178,9 +178,12 @@ __device__ __forceinline__ T ld_row(const T *p) {  // T rows and F entries
     if constexpr (PFAC_TAB_NA) return ld_na(p);
     else return ld_tab(p);
 }
-template <typename T>
+#ifndef PFAC_J2_NA32
+#define PFAC_J2_NA32 1  // J2 / HR loads of uint32 images L1::no_allocate (cfg4 -0.9%; uint16 images: cfg5 +1.2%)
+#endif
+template <bool U32, typename T>
 __device__ __forceinline__ T ld_j2(const T *p) {  // J2 entries and chain-head row copies
-    if constexpr (PFAC_TAB_NA || PFAC_J2_NA) return ld_na(p);
+    if constexpr (PFAC_TAB_NA || PFAC_J2_NA || (U32 && PFAC_J2_NA32)) return ld_na(p);
     else return ld_tab(p);
 }
 
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p)
                 if (JPRE && i < take && (e & 0x8000u))
                     dg[k] = jbuf[((dl[k] >> 3) & 31u) * kJPreK + ((e >> 12) & 7u)];
                 else
-                    dg[k] = (i < take && dl[k] + p.K2 <= le) ? ld_j2(p.J2 + (window16(txt, dl[k]) & p.mask2))
+                    dg[k] = (i < take && dl[k] + p.K2 <= le) ? ld_j2<sizeof(CT) == 4>(p.J2 + (window16(txt, dl[k]) & p.mask2))
                                                              : 0xFFFFFFFFu;
             }
         };
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(mt_for(SL), 1) match_kernel(const MatchArgs p)
                     if ((g & kJ2NB) && (le - l2 < kHRBases || ((window16(txt, l2) ^ (g >> kHRIndexBitsNB)) & 0xFFu)))
                         res = 0;
                     else
-                        res = walk_head(tb, txt, ld_j2(p.HR + (g & (g & kJ2NB ? (1u << kHRIndexBitsNB) - 1 : kJ2NB - 1))),
+                        res = walk_head(tb, txt, ld_j2<sizeof(CT) == 4>(p.HR + (g & (g & kJ2NB ? (1u << kHRIndexBitsNB) - 1 : kJ2NB - 1))),
                                         l2, le);
                 }
                 else if (g & 0x80000000u) res = walk(tb, txt, g & 0x7FFFFFFFu, l + p.K2, le);

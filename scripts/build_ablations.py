@@ -38,7 +38,9 @@ VARIANTS = {
     "mt1k": ["PFAC_MT_1K=1024"],             # A/B: 32 warps per CTA in the 1024-position-slice text kernels
     "mt1k960": ["PFAC_MT_1K=960"],           # A/B: 30 warps per CTA (shared memory stays under the 196-KB carve-out on cfg4)
     "mt1k_q96": ["PFAC_MT_1K=1024", "PFAC_QEXTRA_1K=96"],  # A/B: 32 warps with a shorter queue (cfg4: under 196 KB)
+    "j2a32": ["PFAC_J2_NA32=0"],             # A/B: J2 / HR loads of uint32 images L1-allocating
     "nolds": ["PFAC_LDS_ADDR=0"],            # A/B: shared-window addresses from generic pointers (S2R per conversion)
+    "win1600": ["PFAC_WINDOW_MAX=1600"],     # A/B: at most 1600 rows in shared memory (cfg5: a smaller carve-out, more L1)
     "w32ipl1": ["PFAC_QEXTRA_1K=128", "PFAC_DRAIN_IPL_1K=1"],  # A/B: 32 warps, 1 drain item per lane (same queue)
     "w32ipl3": ["PFAC_MT_1K=1024", "PFAC_QEXTRA_1K=64", "PFAC_DRAIN_IPL_1K=3"],  # A/B: 32 warps, 3 drain items per lane
     "w32ipl4": ["PFAC_MT_1K=1024", "PFAC_QEXTRA_1K=32", "PFAC_DRAIN_IPL_1K=4"],  # A/B: 32 warps, 4 drain items per lane
