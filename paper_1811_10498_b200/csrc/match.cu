@@ -179,7 +179,8 @@ __device__ __forceinline__ T ld_row(const T *p) {  // T rows and F entries
     else return ld_tab(p);
 }
 #ifndef PFAC_J2_NA32
-#define PFAC_J2_NA32 1  // J2 / HR loads of uint32 images L1::no_allocate (cfg4 -0.9%; uint16 images: cfg5 +1.2%)
+#define PFAC_J2_NA32 0  // A/B knob: J2 / HR loads of uint32 images L1::no_allocate (cfg4 -0.9% warm,
+                        // but a cold L2 (ncu replay) then re-reads J2 from DRAM: 2.15x the algorithmic bytes)
 #endif
 template <bool U32, typename T>
 __device__ __forceinline__ T ld_j2(const T *p) {  // J2 entries and chain-head row copies
